@@ -1,0 +1,97 @@
+"""Loading the committed reference fixtures (tests/golden/*, made by make_golden.py)."""
+
+import json
+import os
+
+import numpy as np
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+_TUPLE_KEYS = ("shape", "perm", "starts", "stops", "steps", "stride", "padding", "x_shape", "w_shape")
+
+
+def _restore(params, arrays):
+    p = {}
+    for k, v in params.items():
+        if k in _TUPLE_KEYS and v is not None:
+            v = tuple(v)
+        elif k == "pad_width":
+            v = tuple(tuple(x) for x in v)
+        elif k == "array":
+            v = arrays[v]
+        p[k] = v
+    return p
+
+
+def op_cases():
+    with open(os.path.join(GOLD, "ops.json")) as f:
+        cases = json.load(f)
+    arrays = np.load(os.path.join(GOLD, "ops.npz"))
+    out = []
+    for i, c in enumerate(cases):
+        c = dict(c)
+        c["id"] = f"{i}:{c['name']}:{c.get('tag', '')}"
+        c["params"] = _restore(c["params"], arrays)
+        c["input_arrays"] = [arrays[k] for k in c["inputs"]]
+        c["expected"] = arrays[c["out"]] if "out" in c else None
+        out.append(c)
+    return out
+
+
+def models_meta():
+    with open(os.path.join(GOLD, "models.json")) as f:
+        return json.load(f)
+
+
+def models_arrays():
+    return np.load(os.path.join(GOLD, "models.npz"))
+
+
+def alloc_meta():
+    with open(os.path.join(GOLD, "alloc.json")) as f:
+        return json.load(f)
+
+
+def trace_lines():
+    with open(os.path.join(GOLD, "trace.txt")) as f:
+        return [line.rstrip("\n") for line in f if line.strip()]
+
+
+def rng_arrays():
+    return np.load(os.path.join(GOLD, "rng.npz"))
+
+
+def rel_err(a, b):
+    """The reference's metric |a-b|/max(|a|,|b|,1) (T/test_acceptance.py:260-262)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.size == 0:
+        return 0.0
+    both_nan = np.isnan(a) & np.isnan(b)
+    same_inf = np.isinf(a) & np.isinf(b) & (np.sign(a) == np.sign(b))
+    with np.errstate(invalid="ignore"):
+        d = np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1.0)
+    d = np.where(both_nan | same_inf, 0.0, d)
+    d = np.where(np.isnan(d), np.inf, d)
+    return float(d.max())
+
+
+# per-op tolerance: bit-exact for integer/bool/index/movement/creation, rel 1e-5 float
+EXACT_OPS = {"eq", "lt", "gt", "logical_and", "logical_or", "logical_not", "argmax", "reshape",
+             "transpose", "concat", "slice", "pad", "full", "arange", "from_host", "neg", "abs",
+             "max_reduce", "min_reduce", "minimum", "maximum", "add", "sub", "mul", "div", "sqrt"}
+
+
+def check_against(case, got, tol=1e-5):
+    exp = case["expected"]
+    assert got.dtype == exp.dtype, (case["id"], got.dtype, exp.dtype)
+    assert got.shape == exp.shape, (case["id"], got.shape, exp.shape)
+    if exp.dtype.kind in "biu":
+        assert np.array_equal(got, exp), case["id"]
+        return
+    if case["name"] in EXACT_OPS or case["name"] == "rand_uniform":
+        # IEEE-exact ops are bit-exact whenever numpy computed in the output dtype
+        same = all(a.dtype == exp.dtype for a in case["input_arrays"])
+        if same or case["name"] not in ("add", "sub", "mul", "div"):
+            assert np.array_equal(got, exp, equal_nan=True), (case["id"], got, exp)
+            return
+    assert rel_err(got, exp) <= tol, (case["id"], rel_err(got, exp))
