@@ -1,0 +1,146 @@
+/*
+ * paper_b200.h — C ABI of libpaper_b200.so, the B200 backend behind the Flashlight
+ * (arXiv 2201.12465) reference's primitive table.
+ *
+ * The reference's drop-in boundary is Python: ``Backend.execute(OpCall, adapters)``
+ * (minml/registry.py:97-141; template minml/eager.py:33-64) dispatching to one numpy
+ * kernel per primitive (minml/kernels.py:272-314) with one managed allocation per op
+ * (minml/memory.py:126-157).  Each entry point below replaces one row of that table;
+ * the Python GpuBackend (paper_2201_12465_b200/gpu/backend.py) binds them with ctypes.
+ * INTEGRATION.md shows the equivalent ctypes stub a reference maintainer would add.
+ *
+ * Conventions: every function returns 0 on success or a nonzero pb_status; the text of
+ * the last error on the calling thread is pb_last_error().  Device pointers travel as
+ * uint64_t.  Kernels are enqueued on the backend's compute stream (pb_stream(0)) and
+ * never block, except the documented host transfers / checks.  No torch types appear.
+ */
+#ifndef PAPER_B200_H
+#define PAPER_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum pb_status { PB_OK = 0, PB_ERR_CUDA = 1, PB_ERR_ARG = 2, PB_ERR_OOM = 3, PB_ERR_ALLOC = 4,
+                 PB_ERR_DOMAIN = 5, PB_ERR_NCCL = 6, PB_ERR_UNSUPPORTED = 7 };
+
+/* element types; codes equal the reference's promotion rank (minml/dtypes.py:41-46) */
+enum pb_dtype { PB_BOOL = 0, PB_U8 = 1, PB_I32 = 2, PB_I64 = 3, PB_F32 = 4, PB_F64 = 5 };
+
+#define PB_MAX_RANK 8
+
+/* A strided view: element (i0..in-1) lives at ptr + sum(ik * strides[k]) * itemsize. */
+typedef struct pb_tensor {
+  uint64_t ptr;
+  int32_t dtype;
+  int32_t ndim;
+  int64_t shape[PB_MAX_RANK];
+  int64_t strides[PB_MAX_RANK]; /* in elements; 0 marks a broadcast axis */
+} pb_tensor;
+
+/* A weak Python scalar operand (minml/_tensor.py:90-102, kernels.py:35-42). */
+typedef struct pb_scalar {
+  int32_t kind; /* 0 float (f), 1 int (i), 2 bool (i) */
+  int32_t pad_;
+  double f;
+  int64_t i;
+} pb_scalar;
+
+/* ---- runtime --------------------------------------------------------------------- */
+int pb_init(int device);                 /* select device, create streams */
+int pb_device_count(void);               /* 0 when no device / driver */
+const char* pb_last_error(void);
+int pb_synchronize(void);                /* wait for the compute stream */
+uint64_t pb_stream(int which);           /* 0 compute, 1 comm, 2 copy (cudaStream_t) */
+int pb_h2d(uint64_t dst, const void* src, uint64_t nbytes); /* pinned staging, async */
+int pb_d2h(void* dst, uint64_t src, uint64_t nbytes);       /* blocking */
+int pb_d2d(uint64_t dst, uint64_t src, uint64_t nbytes);    /* async */
+int pb_event_record(int stream_from, int stream_to);        /* stream_to waits on stream_from */
+int pb_graph_begin(void);                 /* start capturing the compute stream */
+int pb_graph_end(uint64_t* graph_exec);   /* finish capture, instantiate */
+int pb_graph_launch(uint64_t graph_exec);
+int pb_graph_destroy(uint64_t graph_exec);
+int pb_timer(int op, uint64_t* handle, float* ms); /* 0 create+record start,1 record stop,2 elapsed,3 destroy */
+
+/* ---- caching device allocator (replaces minml/memory.py:86-347) ------------------- */
+enum pb_policy { PB_POLICY_NATIVE = 0, PB_POLICY_CACHING = 1, PB_POLICY_SPLIT = 2 };
+typedef struct pb_mm_stats {
+  uint64_t live_bytes_requested, live_bytes_granted, peak_granted, cache_bytes;
+  uint64_t alloc_count, free_count, internal_fragmentation, peak_internal_fragmentation;
+  uint64_t live_blocks;
+  double external_fragmentation_ratio;
+} pb_mm_stats;
+typedef struct pb_mm_block {
+  uint64_t id, ptr, requested_bytes, granted_bytes, bin_size;
+  int32_t op_tag, pool;
+} pb_mm_block;
+
+void* pb_mm_create(int policy, uint64_t split_threshold, uint64_t capacity /*0 = none*/, int simulate);
+void pb_mm_destroy(void* mm);
+int pb_mm_alloc(void* mm, uint64_t nbytes, int32_t op_tag, pb_mm_block* out);
+int pb_mm_free(void* mm, uint64_t block_id);
+int pb_mm_record_stream(void* mm, uint64_t block_id, int stream);
+int pb_mm_stats_get(void* mm, pb_mm_stats* out);
+uint64_t pb_mm_flush(void* mm);          /* returns cached blocks released */
+int pb_mm_pool(void* mm, int pool);      /* route allocations to a private pool (graphs); 0 = default */
+uint64_t pb_bin_size(uint64_t nbytes);
+uint64_t pb_round_up(uint64_t nbytes);
+
+/* ---- primitive kernels (minml/kernels.py) ------------------------------------------ */
+enum pb_binop { PB_ADD = 0, PB_SUB, PB_MUL, PB_DIV, PB_POW, PB_MIN, PB_MAX, PB_EQ, PB_LT, PB_GT,
+                PB_AND, PB_OR };
+enum pb_unop { PB_NEG = 0, PB_ABS, PB_EXP, PB_LOG, PB_SQRT, PB_SIN, PB_COS, PB_TANH, PB_NOT, PB_CAST };
+enum pb_redop { PB_SUM = 0, PB_RMAX, PB_RMIN, PB_ARGMAX };
+
+/* out = op(a, b) computed in dtype `compute` (numpy's result type), cast to out->dtype.
+ * Either operand may be replaced by a scalar: pass a == NULL or b == NULL plus `s`. */
+int pb_binary(int op, const pb_tensor* a, const pb_tensor* b, const pb_scalar* s, int compute,
+              const pb_tensor* out);                                    /* kernels.py:88-113 */
+int pb_unary(int op, const pb_tensor* a, int compute, const pb_tensor* out); /* kernels.py:119-129 */
+int pb_copy(const pb_tensor* src, const pb_tensor* dst);   /* strided copy + cast: reshape/transpose/slice/concat */
+int pb_pad(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, const pb_tensor* out); /* :265-269 */
+int pb_fill(const pb_tensor* out, const pb_scalar* value);                /* kernels.py:54-58 */
+int pb_arange(const pb_tensor* out);                                      /* kernels.py:61-62 */
+int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out); /* kernels.py:65-74, rng.py */
+int pb_reduce(int op, const pb_tensor* a, int axis /* -1 = all */, const pb_tensor* out); /* :139-160 */
+int pb_check(int what, const pb_tensor* a, int32_t* result); /* 0: any zero, 1: any negative (blocking) */
+int pb_matmul(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out); /* kernels.py:166-173 */
+typedef struct pb_conv {
+  int32_t stride_h, stride_w, pad_h, pad_w;
+} pb_conv;
+int pb_conv2d(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias /* nullable */,
+              const pb_conv* p, const pb_tensor* out);                     /* kernels.py:197-210 */
+int pb_conv2d_grad_input(const pb_tensor* g, const pb_tensor* w, const pb_conv* p,
+                         const pb_tensor* out);                            /* kernels.py:213-228 */
+int pb_conv2d_grad_weight(const pb_tensor* x, const pb_tensor* g, const pb_conv* p,
+                          const pb_tensor* out);                           /* kernels.py:231-239 */
+/* In-place multi-tensor SGD (minml/optim.py:64-72 op for op): for each i,
+ * g' = g + wd*p (if wd); v = v*mu + g' (if mu, else v := g'); p = p - v*lr.  f32 only. */
+int pb_sgd(int n, const uint64_t* params_in, const uint64_t* params_out, const uint64_t* grads,
+           const uint64_t* vels_in, const uint64_t* vels_out, const int64_t* numels, float lr,
+           float momentum, float weight_decay);  /* out may alias in (in-place update) */
+/* Pack / unpack gradient buckets (data-parallel sync) and scale by 1/world. */
+int pb_bucket_pack(int n, const uint64_t* srcs, const int64_t* numels, uint64_t bucket);
+int pb_scale_f32(uint64_t buf, int64_t n, float divisor); /* buf[i] = buf[i] / divisor */
+
+/* ---- NCCL (replaces minml/distributed.py:129-175) ---------------------------------- */
+int pb_nccl_unique_id(uint8_t out[128]);
+void* pb_nccl_init(int nranks, int rank, const uint8_t id[128]);
+int pb_nccl_destroy(void* comm);
+/* op: 0 sum, 1 max, 2 avg; dtype pb_dtype; runs on the comm stream after a fence on compute */
+int pb_nccl_allreduce(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t count, int dtype, int op);
+int pb_nccl_broadcast(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t count, int dtype, int root);
+int pb_nccl_allgather(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t count, int dtype);
+int pb_nccl_wait(void* comm);  /* compute stream waits for everything enqueued on the comm stream */
+
+/* ---- introspection ------------------------------------------------------------------ */
+uint64_t pb_launch_count(void);  /* kernels launched by this library so far */
+int pb_gemm_path(void);          /* 1 when the tcgen05 path is enabled, 0 = SIMT */
+int pb_set_gemm_path(int tc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,696 @@
+// Elementwise primitives: broadcast binary ops, unary ops, casts, strided copies
+// (reshape / transpose / slice / concat materialisation), pad, fill, arange, checks,
+// and the fused multi-tensor SGD update.  Semantics: minml/kernels.py:25-129, 245-269.
+//
+// Numerics: every op computes in numpy's result type `CT` (chosen on the host), is
+// compiled with -fmad=false, and uses IEEE-rounded division/sqrt, so + - * / sqrt and
+// all integer/bool/compare/movement ops are bit-exact against numpy; transcendental ops
+// use CUDA's libm (<= 2 ulp).
+//
+// Kernels (all HBM-bound; algorithmic bytes = sum of operand + output bytes):
+//   ew_vec   contiguous operands (or a scalar), 16-byte vector loads/stores, grid-stride
+//            sized to SMs*resident blocks.
+//   ew_rows  any strides: the innermost axis is walked with unit steps per thread
+//            (coalesced when it is contiguous), outer axes are decomposed once per tile.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <type_traits>
+#include <vector>
+#include "common.cuh"
+
+namespace pb {
+
+// ---------------------------------------------------------------------------- operators
+template <typename T> __device__ __forceinline__ bool isnan_(T) { return false; }
+template <> __device__ __forceinline__ bool isnan_(float v) { return v != v; }
+template <> __device__ __forceinline__ bool isnan_(double v) { return v != v; }
+
+template <typename T>
+__device__ __forceinline__ T ipow(T base, T e) {
+  T r = 1;
+  while (e > 0) {
+    if (e & 1) r = (T)(r * base);
+    base = (T)(base * base);
+    e >>= 1;
+  }
+  return r;
+}
+__device__ __forceinline__ float pow_(float a, float b) { return powf(a, b); }
+__device__ __forceinline__ double pow_(double a, double b) { return pow(a, b); }
+__device__ __forceinline__ int32_t pow_(int32_t a, int32_t b) { return ipow<int32_t>(a, b); }
+__device__ __forceinline__ int64_t pow_(int64_t a, int64_t b) { return ipow<int64_t>(a, b); }
+__device__ __forceinline__ uint8_t pow_(uint8_t a, uint8_t b) { return (uint8_t)ipow<uint32_t>(a, b); }
+__device__ __forceinline__ bool pow_(bool a, bool b) { return a || !b; }
+
+template <int OP, typename T>
+struct Bin;
+#define PB_BIN(OPC, R, EXPR)                                                  \
+  template <typename T>                                                       \
+  struct Bin<OPC, T> {                                                        \
+    typedef R res;                                                            \
+    __device__ __forceinline__ static R f(T a, T b) { return EXPR; }         \
+  };
+PB_BIN(PB_ADD, T, (T)(a + b))
+PB_BIN(PB_SUB, T, (T)(a - b))
+PB_BIN(PB_MUL, T, (T)(a * b))
+PB_BIN(PB_DIV, T, (T)(a / b))
+PB_BIN(PB_POW, T, pow_(a, b))
+PB_BIN(PB_MIN, T, (isnan_(a) || a <= b) ? a : b)
+PB_BIN(PB_MAX, T, (isnan_(a) || a >= b) ? a : b)
+PB_BIN(PB_EQ, bool, a == b)
+PB_BIN(PB_LT, bool, a < b)
+PB_BIN(PB_GT, bool, a > b)
+PB_BIN(PB_AND, bool, (bool)a && (bool)b)
+PB_BIN(PB_OR, bool, (bool)a || (bool)b)
+#undef PB_BIN
+
+template <typename T> __device__ __forceinline__ T neg_(T v) { return (T)(-v); }
+template <> __device__ __forceinline__ bool neg_(bool v) { return v; }
+template <typename T> __device__ __forceinline__ T abs_(T v) { return v < 0 ? (T)(-v) : v; }
+template <> __device__ __forceinline__ float abs_(float v) { return fabsf(v); }
+template <> __device__ __forceinline__ double abs_(double v) { return fabs(v); }
+template <> __device__ __forceinline__ uint8_t abs_(uint8_t v) { return v; }
+template <> __device__ __forceinline__ bool abs_(bool v) { return v; }
+
+template <typename T> __device__ __forceinline__ T fexp(T v) { return (T)exp((double)v); }
+__device__ __forceinline__ float fexp(float v) { return expf(v); }
+template <typename T> __device__ __forceinline__ T flog(T v) { return (T)log((double)v); }
+__device__ __forceinline__ float flog(float v) { return logf(v); }
+template <typename T> __device__ __forceinline__ T fsqrt(T v) { return (T)sqrt((double)v); }
+__device__ __forceinline__ float fsqrt(float v) { return sqrtf(v); }
+template <typename T> __device__ __forceinline__ T fsin(T v) { return (T)sin((double)v); }
+__device__ __forceinline__ float fsin(float v) { return sinf(v); }
+template <typename T> __device__ __forceinline__ T fcos(T v) { return (T)cos((double)v); }
+__device__ __forceinline__ float fcos(float v) { return cosf(v); }
+template <typename T> __device__ __forceinline__ T ftanh(T v) { return (T)tanh((double)v); }
+__device__ __forceinline__ float ftanh(float v) { return tanhf(v); }
+
+template <int OP, typename T>
+struct Un {
+  typedef T res;
+  __device__ __forceinline__ static T f(T v) {
+    switch (OP) {
+      case PB_NEG: return neg_(v);
+      case PB_ABS: return abs_(v);
+      case PB_EXP: return fexp(v);
+      case PB_LOG: return flog(v);
+      case PB_SQRT: return fsqrt(v);
+      case PB_SIN: return fsin(v);
+      case PB_COS: return fcos(v);
+      case PB_TANH: return ftanh(v);
+      case PB_NOT: return (T)(!(bool)v);
+      default: return v;  // PB_CAST: value already converted by load_as
+    }
+  }
+};
+
+// ------------------------------------------------------------------------ vector path
+template <typename T> struct Vec { static const int N = 16 / sizeof(T); };
+
+template <typename T, int N>
+struct alignas(16) Pack {
+  T v[N];
+};
+template <typename R, int N>
+struct alignas(sizeof(R) * N >= 16 ? 16 : sizeof(R) * N) OutPack {
+  R v[N];
+};
+
+// binary: a/b either full arrays (mode 0) or a scalar (mode 1); out contiguous
+template <int OP, typename T, typename R, int AM, int BM>
+__global__ void __launch_bounds__(256) ew_vec_bin(const T* __restrict__ a, const T* __restrict__ b, T sa, T sb,
+                                                  R* __restrict__ out, int64_t n) {
+  const int N = Vec<T>::N;
+  int64_t nv = n / N;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    Pack<T, N> pa, pb_;
+    if (AM == 0) pa = reinterpret_cast<const Pack<T, N>*>(a)[i];
+    if (BM == 0) pb_ = reinterpret_cast<const Pack<T, N>*>(b)[i];
+    OutPack<R, N> o;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      T x = AM == 0 ? pa.v[k] : sa;
+      T y = BM == 0 ? pb_.v[k] : sb;
+      o.v[k] = cvt<R>(Bin<OP, T>::f(x, y));
+    }
+    *reinterpret_cast<OutPack<R, N>*>(out + i * N) = o;
+  }
+  for (int64_t i = nv * N + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    T x = AM == 0 ? a[i] : sa;
+    T y = BM == 0 ? b[i] : sb;
+    out[i] = cvt<R>(Bin<OP, T>::f(x, y));
+  }
+}
+
+template <int OP, typename T, typename R>
+__global__ void __launch_bounds__(256) ew_vec_un(const T* __restrict__ a, R* __restrict__ out, int64_t n) {
+  const int N = Vec<T>::N;
+  int64_t nv = n / N;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    Pack<T, N> pa = reinterpret_cast<const Pack<T, N>*>(a)[i];
+    OutPack<R, N> o;
+#pragma unroll
+    for (int k = 0; k < N; ++k) o.v[k] = cvt<R>(Un<OP, T>::f(pa.v[k]));
+    *reinterpret_cast<OutPack<R, N>*>(out + i * N) = o;
+  }
+  for (int64_t i = nv * N + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = cvt<R>(Un<OP, T>::f(a[i]));
+}
+
+// -------------------------------------------------------------------------- rows path
+struct RowArgs {
+  const void* a;
+  const void* b;
+  void* out;
+  int dta, dtb, dto;
+  Dims d;         // coalesced; st[0]=a, st[1]=b, st[2]=out
+  int64_t inner;  // extent of the last axis
+  int64_t rows;
+  int64_t tiles;  // tiles per row
+};
+
+static const int kRowTile = 2048;
+
+template <typename F>
+__device__ __forceinline__ void row_walk(const RowArgs& r, F&& body) {
+  const int nd = r.d.ndim;
+  for (int64_t t = blockIdx.x; t < r.rows * r.tiles; t += gridDim.x) {
+    int64_t row = t / r.tiles;
+    int64_t c0 = (t - row * r.tiles) * kRowTile;
+    int64_t oa = 0, ob = 0, oo = 0;
+    if (r.rows <= 0x7fffffff) {
+      uint32_t rr = (uint32_t)row;
+      for (int k = nd - 2; k >= 0; --k) {
+        uint32_t ext = (uint32_t)r.d.shape[k];
+        uint32_t q = rr / ext;
+        int64_t idx = rr - q * ext;
+        rr = q;
+        oa += idx * r.d.st[0][k];
+        ob += idx * r.d.st[1][k];
+        oo += idx * r.d.st[2][k];
+      }
+    } else {
+      int64_t rr = row;
+      for (int k = nd - 2; k >= 0; --k) {
+        int64_t ext = r.d.shape[k];
+        int64_t idx = rr % ext;
+        rr /= ext;
+        oa += idx * r.d.st[0][k];
+        ob += idx * r.d.st[1][k];
+        oo += idx * r.d.st[2][k];
+      }
+    }
+    const int64_t sa = r.d.st[0][nd - 1], sb = r.d.st[1][nd - 1], so = r.d.st[2][nd - 1];
+    int64_t cend = c0 + kRowTile < r.inner ? c0 + kRowTile : r.inner;
+    for (int64_t c = c0 + threadIdx.x; c < cend; c += blockDim.x) body(oa + c * sa, ob + c * sb, oo + c * so);
+  }
+}
+
+template <int OP, typename CT>
+__global__ void __launch_bounds__(256) ew_rows_bin(RowArgs r, CT sa, CT sb, int am, int bm) {
+  typedef typename Bin<OP, CT>::res R;
+  row_walk(r, [&](int64_t ia, int64_t ib, int64_t io) {
+    CT x = am ? sa : load_as<CT>(r.a, r.dta, ia);
+    CT y = bm ? sb : load_as<CT>(r.b, r.dtb, ib);
+    store_from<R>(r.out, r.dto, io, Bin<OP, CT>::f(x, y));
+  });
+}
+
+template <int OP, typename CT>
+__global__ void __launch_bounds__(256) ew_rows_un(RowArgs r) {
+  row_walk(r, [&](int64_t ia, int64_t, int64_t io) {
+    store_from<CT>(r.out, r.dto, io, Un<OP, CT>::f(load_as<CT>(r.a, r.dta, ia)));
+  });
+}
+
+// ----------------------------------------------------------------------- host helpers
+static void fill_dims(Dims& d, const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
+  d.ndim = out->ndim;
+  for (int k = 0; k < out->ndim; ++k) {
+    d.shape[k] = out->shape[k];
+    d.st[2][k] = out->strides[k];
+    d.st[0][k] = 0;
+    d.st[1][k] = 0;
+  }
+  // right-align operands; broadcast axes (extent 1) get stride 0
+  const pb_tensor* ops[2] = {a, b};
+  for (int o = 0; o < 2; ++o) {
+    const pb_tensor* t = ops[o];
+    if (!t) continue;
+    int off = out->ndim - t->ndim;
+    for (int k = 0; k < t->ndim; ++k) d.st[o][off + k] = (t->shape[k] == 1) ? 0 : t->strides[k];
+  }
+}
+
+static RowArgs make_rows(const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
+  RowArgs r;
+  r.a = a ? (const void*)(uintptr_t)a->ptr : nullptr;
+  r.b = b ? (const void*)(uintptr_t)b->ptr : nullptr;
+  r.out = (void*)(uintptr_t)out->ptr;
+  r.dta = a ? a->dtype : 0;
+  r.dtb = b ? b->dtype : 0;
+  r.dto = out->dtype;
+  fill_dims(r.d, out, a, b);
+  coalesce(r.d, 3);
+  r.inner = r.d.shape[r.d.ndim - 1];
+  r.rows = 1;
+  for (int k = 0; k < r.d.ndim - 1; ++k) r.rows *= r.d.shape[k];
+  r.tiles = (r.inner + kRowTile - 1) / kRowTile;
+  return r;
+}
+
+static int rows_grid(const RowArgs& r) {
+  int64_t units = r.rows * r.tiles;
+  int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(units < cap ? (units < 1 ? 1 : units) : cap);
+}
+
+static bool aligned16(uint64_t p) { return (p & 15) == 0; }
+
+// full-array (same linear index as out) or scalar-like (all strides 0)
+static int vec_mode(const pb_tensor* t, const pb_tensor* out) {
+  if (!t) return 1;
+  bool zero = true;
+  for (int k = 0; k < t->ndim; ++k)
+    if (t->shape[k] != 1 && t->strides[k] != 0) zero = false;
+  if (zero) return 1;
+  if (t->ndim != out->ndim) return -1;
+  for (int k = 0; k < t->ndim; ++k)
+    if (t->shape[k] != out->shape[k]) return -1;
+  return is_contiguous(*t) && aligned16(t->ptr) ? 0 : -1;
+}
+
+template <typename T>
+static T read_scalar_host(const pb_tensor* t, bool* ok);
+
+template <int OP, typename T, typename R>
+static int launch_vec_bin(const pb_tensor* a, const pb_tensor* b, int am, int bm, T sa, T sb, const pb_tensor* out,
+                          int64_t n) {
+  const T* pa = a ? (const T*)(uintptr_t)a->ptr : nullptr;
+  const T* pb2 = b ? (const T*)(uintptr_t)b->ptr : nullptr;
+  R* po = (R*)(uintptr_t)out->ptr;
+  int grid = grid_for(n, 256, Vec<T>::N * 2);
+  cudaStream_t s = compute_stream();
+  if (am == 0 && bm == 0) ew_vec_bin<OP, T, R, 0, 0><<<grid, 256, 0, s>>>(pa, pb2, sa, sb, po, n);
+  else if (am == 0) ew_vec_bin<OP, T, R, 0, 1><<<grid, 256, 0, s>>>(pa, pb2, sa, sb, po, n);
+  else ew_vec_bin<OP, T, R, 1, 0><<<grid, 256, 0, s>>>(pa, pb2, sa, sb, po, n);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+template <int OP, typename CT>
+static int run_binary(const pb_tensor* a, const pb_tensor* b, const pb_scalar* s, const pb_tensor* out) {
+  typedef typename Bin<OP, CT>::res R;
+  int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  CT sa = 0, sb = 0;
+  int am = a ? 0 : 1, bm = b ? 0 : 1;
+  if (!a) sa = scalar_as<CT>(s);
+  if (!b) sb = scalar_as<CT>(s);
+  // vector fast path: operand dtypes == CT, out dtype == R, contiguous / scalar
+  const int ct = std::is_same<CT, float>::value ? PB_F32 : std::is_same<CT, bool>::value ? PB_BOOL : -1;
+  const int rt = std::is_same<R, float>::value ? PB_F32 : std::is_same<R, bool>::value ? PB_BOOL : -2;
+  if (ct >= 0 && out->dtype == rt && is_contiguous(*out) && aligned16(out->ptr) && (!a || a->dtype == ct) &&
+      (!b || b->dtype == ct)) {
+    int va = vec_mode(a, out), vb = vec_mode(b, out);
+    if (va >= 0 && vb >= 0 && !(va == 1 && vb == 1)) {
+      // a broadcast-to-all tensor operand becomes a scalar; read it from its single element
+      if (a && va == 1) {
+        RowArgs r = make_rows(out, a, b);
+        ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, 0, 0);
+        PB_LAUNCHED();
+        return PB_OK;
+      }
+      if (b && vb == 1) {
+        RowArgs r = make_rows(out, a, b);
+        ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, 0, 0);
+        PB_LAUNCHED();
+        return PB_OK;
+      }
+      return launch_vec_bin<OP, CT, R>(a, b, va, vb, sa, sb, out, n);
+    }
+  }
+  RowArgs r = make_rows(out, a, b);
+  ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, am, bm);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+template <int OP>
+static int dispatch_binary(int compute, const pb_tensor* a, const pb_tensor* b, const pb_scalar* s,
+                           const pb_tensor* out) {
+  switch (compute) {
+    case PB_BOOL: return run_binary<OP, bool>(a, b, s, out);
+    case PB_U8: return run_binary<OP, uint8_t>(a, b, s, out);
+    case PB_I32: return run_binary<OP, int32_t>(a, b, s, out);
+    case PB_I64: return run_binary<OP, int64_t>(a, b, s, out);
+    case PB_F32: return run_binary<OP, float>(a, b, s, out);
+    case PB_F64: return run_binary<OP, double>(a, b, s, out);
+  }
+  return fail(PB_ERR_ARG, "pb_binary: bad compute dtype");
+}
+
+template <int OP, typename CT>
+static int run_unary(const pb_tensor* a, const pb_tensor* out) {
+  int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  const int ct = std::is_same<CT, float>::value ? PB_F32 : std::is_same<CT, bool>::value ? PB_BOOL : -1;
+  if (ct >= 0 && a->dtype == ct && out->dtype == ct && is_contiguous(*a) && is_contiguous(*out) &&
+      aligned16(a->ptr) && aligned16(out->ptr)) {
+    ew_vec_un<OP, CT, CT><<<grid_for(n, 256, Vec<CT>::N * 2), 256, 0, compute_stream()>>>(
+        (const CT*)(uintptr_t)a->ptr, (CT*)(uintptr_t)out->ptr, n);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
+  RowArgs r = make_rows(out, a, nullptr);
+  ew_rows_un<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+template <int OP>
+static int dispatch_unary(int compute, const pb_tensor* a, const pb_tensor* out) {
+  switch (compute) {
+    case PB_BOOL: return run_unary<OP, bool>(a, out);
+    case PB_U8: return run_unary<OP, uint8_t>(a, out);
+    case PB_I32: return run_unary<OP, int32_t>(a, out);
+    case PB_I64: return run_unary<OP, int64_t>(a, out);
+    case PB_F32: return run_unary<OP, float>(a, out);
+    case PB_F64: return run_unary<OP, double>(a, out);
+  }
+  return fail(PB_ERR_ARG, "pb_unary: bad compute dtype");
+}
+
+// cast: bool -> f32 and f32 -> bool are on the ReLU-mask hot path; give them vector kernels
+static int run_cast(const pb_tensor* src, const pb_tensor* dst) {
+  int64_t n = numel(*dst);
+  if (n == 0) return PB_OK;
+  bool contig = is_contiguous(*src) && is_contiguous(*dst) && aligned16(src->ptr) && aligned16(dst->ptr) &&
+                src->ndim == dst->ndim;
+  if (contig && src->dtype == PB_BOOL && dst->dtype == PB_F32) {
+    ew_vec_un<PB_CAST, bool, float><<<grid_for(n, 256, 32), 256, 0, compute_stream()>>>(
+        (const bool*)(uintptr_t)src->ptr, (float*)(uintptr_t)dst->ptr, n);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
+  if (contig && src->dtype == dst->dtype && src->dtype == PB_F32) {
+    ew_vec_un<PB_CAST, float, float><<<grid_for(n, 256, 8), 256, 0, compute_stream()>>>(
+        (const float*)(uintptr_t)src->ptr, (float*)(uintptr_t)dst->ptr, n);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
+  return dispatch_unary<PB_CAST>(dst->dtype, src, dst);
+}
+
+// ---------------------------------------------------------------------------- pad / fill
+struct PadArgs {
+  const void* src;
+  void* out;
+  int dts, dto, ndim;
+  int64_t oshape[PB_MAX_RANK], ostr[PB_MAX_RANK], sshape[PB_MAX_RANK], sstr[PB_MAX_RANK], lo[PB_MAX_RANK];
+  int64_t n;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) pad_kernel(PadArgs p, T value) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = i, so = 0, oo = 0;
+    bool inside = true;
+    for (int k = p.ndim - 1; k >= 0; --k) {
+      int64_t idx = rem % p.oshape[k];
+      rem /= p.oshape[k];
+      oo += idx * p.ostr[k];
+      int64_t j = idx - p.lo[k];
+      if (j < 0 || j >= p.sshape[k]) inside = false;
+      so += j * p.sstr[k];
+    }
+    T v = inside ? load_as<T>(p.src, p.dts, so) : value;
+    store_from<T>(p.out, p.dto, oo, v);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) fill_kernel(T* out, int64_t n, T v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+__global__ void arange_kernel(int64_t* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = i;
+}
+
+template <typename T>
+__global__ void check_kernel(const void* p, int dt, RowArgs r, int what, int32_t* flag) {
+  row_walk(r, [&](int64_t ia, int64_t, int64_t) {
+    T v = load_as<T>(p, dt, ia);
+    if ((what == 0 && v == 0) || (what == 1 && v < 0)) *flag = 1;
+  });
+}
+
+// ---------------------------------------------------------------------- fused SGD step
+// Multi-tensor launches carry their tensor table in the kernel parameters (no host->device
+// metadata copies, so the launch is CUDA-graph capturable).  Each tensor is cut into
+// 8192-element work items; blocks find their tensor by binary search over item prefixes.
+static const int kMaxTensors = 128;
+static const int64_t kItem = 8192;
+struct MultiTable {
+  float* p[kMaxTensors];        // parameter out (may equal pin)
+  const float* pin[kMaxTensors];
+  const float* g[kMaxTensors];
+  float* v[kMaxTensors];        // velocity out (may equal vin)
+  const float* vin[kMaxTensors];
+  int64_t n[kMaxTensors];
+  int64_t dst[kMaxTensors];    // bucket offsets (pack)
+  int32_t first[kMaxTensors + 1];  // prefix of work items
+  int count;
+};
+
+__device__ __forceinline__ int find_tensor(const MultiTable& t, int item) {
+  int lo = 0, hi = t.count - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (t.first[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// op order matches minml/optim.py:24-33, 64-72, each op rounded separately (no FMA):
+//   g' = g + p*wd ; v = v*mu + g' ; p = p - v*lr
+__global__ void __launch_bounds__(256) sgd_kernel(const __grid_constant__ MultiTable t, float lr, float mu, float wd,
+                                                  int has_mu, int has_wd) {
+  int items = t.first[t.count];
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int k = find_tensor(t, it);
+    int64_t s = (int64_t)(it - t.first[k]) * kItem;
+    int64_t e = s + kItem < t.n[k] ? s + kItem : t.n[k];
+    float* P = t.p[k];
+    const float* PI = t.pin[k];
+    const float* G = t.g[k];
+    float* V = t.v[k];
+    const float* VI = t.vin[k];
+    for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) {
+      float g = G[i];
+      float p = PI[i];
+      if (has_wd) g = __fadd_rn(g, __fmul_rn(p, wd));
+      float v = g;
+      if (has_mu) {
+        v = __fadd_rn(__fmul_rn(VI[i], mu), g);
+        V[i] = v;
+      }
+      P[i] = __fsub_rn(p, __fmul_rn(v, lr));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) pack_kernel(const __grid_constant__ MultiTable t, float* bucket) {
+  int items = t.first[t.count];
+  for (int it = blockIdx.x; it < items; it += gridDim.x) {
+    int k = find_tensor(t, it);
+    int64_t s = (int64_t)(it - t.first[k]) * kItem;
+    int64_t e = s + kItem < t.n[k] ? s + kItem : t.n[k];
+    const float* G = t.g[k];
+    float* D = bucket + t.dst[k];
+    for (int64_t i = s + threadIdx.x; i < e; i += blockDim.x) D[i] = G[i];
+  }
+}
+
+__global__ void scale_kernel(float* buf, int64_t n, float div) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = __fdiv_rn(buf[i], div);
+}
+
+}  // namespace pb
+
+using namespace pb;
+
+#define PB_CASE_BIN(OPC) \
+  case OPC: return dispatch_binary<OPC>(compute, a, b, s, out);
+#define PB_CASE_UN(OPC) \
+  case OPC: return dispatch_unary<OPC>(compute, a, out);
+
+extern "C" {
+
+int pb_binary(int op, const pb_tensor* a, const pb_tensor* b, const pb_scalar* s, int compute, const pb_tensor* out) {
+  if ((!a || !b) && !s) return fail(PB_ERR_ARG, "pb_binary: missing scalar operand");
+  switch (op) {
+    PB_CASE_BIN(PB_ADD) PB_CASE_BIN(PB_SUB) PB_CASE_BIN(PB_MUL) PB_CASE_BIN(PB_DIV) PB_CASE_BIN(PB_POW)
+    PB_CASE_BIN(PB_MIN) PB_CASE_BIN(PB_MAX) PB_CASE_BIN(PB_EQ) PB_CASE_BIN(PB_LT) PB_CASE_BIN(PB_GT)
+    PB_CASE_BIN(PB_AND) PB_CASE_BIN(PB_OR)
+  }
+  return fail(PB_ERR_ARG, "pb_binary: unknown op");
+}
+
+int pb_unary(int op, const pb_tensor* a, int compute, const pb_tensor* out) {
+  switch (op) {
+    PB_CASE_UN(PB_NEG) PB_CASE_UN(PB_ABS) PB_CASE_UN(PB_EXP) PB_CASE_UN(PB_LOG) PB_CASE_UN(PB_SQRT)
+    PB_CASE_UN(PB_SIN) PB_CASE_UN(PB_COS) PB_CASE_UN(PB_TANH) PB_CASE_UN(PB_NOT)
+    case PB_CAST: return run_cast(a, out);
+  }
+  return fail(PB_ERR_ARG, "pb_unary: unknown op");
+}
+
+int pb_copy(const pb_tensor* src, const pb_tensor* dst) { return run_cast(src, dst); }
+
+int pb_pad(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, const pb_tensor* out) {
+  PadArgs p;
+  p.src = (const void*)(uintptr_t)src->ptr;
+  p.out = (void*)(uintptr_t)out->ptr;
+  p.dts = src->dtype;
+  p.dto = out->dtype;
+  p.ndim = out->ndim;
+  p.n = numel(*out);
+  if (p.n == 0) return PB_OK;
+  for (int k = 0; k < out->ndim; ++k) {
+    p.oshape[k] = out->shape[k];
+    p.ostr[k] = out->strides[k];
+    p.sshape[k] = src->shape[k];
+    p.sstr[k] = src->strides[k];
+    p.lo[k] = lo[k];
+  }
+  int grid = grid_for(p.n, 256, 4);
+  cudaStream_t st = compute_stream();
+  switch (out->dtype) {
+    case PB_BOOL: pad_kernel<bool><<<grid, 256, 0, st>>>(p, scalar_as<bool>(value)); break;
+    case PB_U8: pad_kernel<uint8_t><<<grid, 256, 0, st>>>(p, scalar_as<uint8_t>(value)); break;
+    case PB_I32: pad_kernel<int32_t><<<grid, 256, 0, st>>>(p, scalar_as<int32_t>(value)); break;
+    case PB_I64: pad_kernel<int64_t><<<grid, 256, 0, st>>>(p, scalar_as<int64_t>(value)); break;
+    case PB_F32: pad_kernel<float><<<grid, 256, 0, st>>>(p, scalar_as<float>(value)); break;
+    default: pad_kernel<double><<<grid, 256, 0, st>>>(p, scalar_as<double>(value)); break;
+  }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+int pb_fill(const pb_tensor* out, const pb_scalar* v) {
+  int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  int grid = grid_for(n, 256, 4);
+  cudaStream_t st = compute_stream();
+  void* p = (void*)(uintptr_t)out->ptr;
+  switch (out->dtype) {
+    case PB_BOOL: fill_kernel<bool><<<grid, 256, 0, st>>>((bool*)p, n, scalar_as<bool>(v)); break;
+    case PB_U8: fill_kernel<uint8_t><<<grid, 256, 0, st>>>((uint8_t*)p, n, scalar_as<uint8_t>(v)); break;
+    case PB_I32: fill_kernel<int32_t><<<grid, 256, 0, st>>>((int32_t*)p, n, scalar_as<int32_t>(v)); break;
+    case PB_I64: fill_kernel<int64_t><<<grid, 256, 0, st>>>((int64_t*)p, n, scalar_as<int64_t>(v)); break;
+    case PB_F32: fill_kernel<float><<<grid, 256, 0, st>>>((float*)p, n, scalar_as<float>(v)); break;
+    default: fill_kernel<double><<<grid, 256, 0, st>>>((double*)p, n, scalar_as<double>(v)); break;
+  }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+int pb_arange(const pb_tensor* out) {
+  int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  if (out->dtype != PB_I64) return fail(PB_ERR_ARG, "pb_arange: i64 only");
+  arange_kernel<<<grid_for(n, 256, 4), 256, 0, compute_stream()>>>((int64_t*)(uintptr_t)out->ptr, n);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+int pb_check(int what, const pb_tensor* a, int32_t* result) {
+  *result = 0;
+  if (numel(*a) == 0) return PB_OK;
+  int32_t* flag = (int32_t*)workspace(16);
+  if (!flag) return fail(PB_ERR_OOM, "pb_check: no workspace");
+  PB_CUDA(cudaMemsetAsync(flag, 0, 4, compute_stream()));
+  RowArgs r = make_rows(a, a, nullptr);
+  if (a->dtype == PB_F32 || a->dtype == PB_F64)
+    check_kernel<double><<<rows_grid(r), 256, 0, compute_stream()>>>(r.a, a->dtype, r, what, flag);
+  else
+    check_kernel<int64_t><<<rows_grid(r), 256, 0, compute_stream()>>>(r.a, a->dtype, r, what, flag);
+  PB_LAUNCHED();
+  PB_CUDA(cudaMemcpyAsync(result, flag, 4, cudaMemcpyDeviceToHost, compute_stream()));
+  PB_CUDA(cudaStreamSynchronize(compute_stream()));
+  return PB_OK;
+}
+
+int pb_sgd(int n, const uint64_t* params_in, const uint64_t* params_out, const uint64_t* grads,
+           const uint64_t* vels_in, const uint64_t* vels_out, const int64_t* numels, float lr, float momentum,
+           float wd) {
+  const uint64_t* vels = vels_out;
+  const uint64_t* params = params_out;
+  for (int base = 0; base < n; base += kMaxTensors) {
+    MultiTable t;
+    t.count = 0;
+    int32_t items = 0;
+    for (int i = base; i < n && t.count < kMaxTensors; ++i) {
+      int k = t.count++;
+      t.p[k] = (float*)(uintptr_t)params[i];
+      t.pin[k] = (const float*)(uintptr_t)params_in[i];
+      t.g[k] = (const float*)(uintptr_t)grads[i];
+      t.v[k] = vels ? (float*)(uintptr_t)vels[i] : nullptr;
+      t.vin[k] = vels_in ? (const float*)(uintptr_t)vels_in[i] : nullptr;
+      t.n[k] = numels[i];
+      t.dst[k] = 0;
+      t.first[k] = items;
+      items += (int32_t)((numels[i] + kItem - 1) / kItem);
+    }
+    t.first[t.count] = items;
+    if (items == 0) continue;
+    int grid = items < num_sms() * 8 ? items : num_sms() * 8;
+    sgd_kernel<<<grid, 256, 0, compute_stream()>>>(t, lr, momentum, wd, momentum != 0.0f && vels, wd != 0.0f);
+    PB_LAUNCHED();
+  }
+  return PB_OK;
+}
+
+int pb_bucket_pack(int n, const uint64_t* srcs, const int64_t* numels, uint64_t bucket) {
+  int64_t acc = 0;
+  for (int base = 0; base < n; base += kMaxTensors) {
+    MultiTable t;
+    t.count = 0;
+    int32_t items = 0;
+    for (int i = base; i < n && t.count < kMaxTensors; ++i) {
+      int k = t.count++;
+      t.p[k] = nullptr;
+      t.pin[k] = nullptr;
+      t.v[k] = nullptr;
+      t.vin[k] = nullptr;
+      t.g[k] = (const float*)(uintptr_t)srcs[i];
+      t.n[k] = numels[i];
+      t.dst[k] = acc;
+      acc += numels[i];
+      t.first[k] = items;
+      items += (int32_t)((numels[i] + kItem - 1) / kItem);
+    }
+    t.first[t.count] = items;
+    if (items == 0) continue;
+    int grid = items < num_sms() * 8 ? items : num_sms() * 8;
+    pack_kernel<<<grid, 256, 0, compute_stream()>>>(t, (float*)(uintptr_t)bucket);
+    PB_LAUNCHED();
+  }
+  return PB_OK;
+}
+
+int pb_scale_f32(uint64_t buf, int64_t n, float divisor) {
+  if (n <= 0) return PB_OK;
+  scale_kernel<<<grid_for(n, 256, 4), 256, 0, compute_stream()>>>((float*)(uintptr_t)buf, n, divisor);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+}  // extern "C"

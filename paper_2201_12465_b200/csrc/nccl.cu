@@ -1,0 +1,96 @@
+// NCCL collectives on device buffers (replaces the thread-rank ring of
+// minml/distributed.py:129-175).  Collectives run on the comm stream after an event fence
+// on the compute stream; pb_nccl_wait makes the compute stream wait for them.
+#include <nccl.h>
+#include <cstring>
+#include "common.cuh"
+
+using namespace pb;
+
+static ncclDataType_t nccl_type(int dt) {
+  switch (dt) {
+    case PB_U8: case PB_BOOL: return ncclUint8;
+    case PB_I32: return ncclInt32;
+    case PB_I64: return ncclInt64;
+    case PB_F32: return ncclFloat32;
+    default: return ncclFloat64;
+  }
+}
+
+#define PB_NCCL(call)                                                                  \
+  do {                                                                                 \
+    ncclResult_t r_ = (call);                                                          \
+    if (r_ != ncclSuccess) return fail(PB_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+static int fence_compute_to_comm() {
+  cudaEvent_t ev;
+  PB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  PB_CUDA(cudaEventRecord(ev, compute_stream()));
+  PB_CUDA(cudaStreamWaitEvent(comm_stream(), ev, 0));
+  PB_CUDA(cudaEventDestroy(ev));
+  return PB_OK;
+}
+
+extern "C" {
+
+int pb_nccl_unique_id(uint8_t out[128]) {
+  ncclUniqueId id;
+  PB_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, id.internal, 128);
+  return PB_OK;
+}
+
+void* pb_nccl_init(int nranks, int rank, const uint8_t id_bytes[128]) {
+  ncclUniqueId id;
+  std::memcpy(id.internal, id_bytes, 128);
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, nranks, id, rank);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    return nullptr;
+  }
+  return (void*)comm;
+}
+
+int pb_nccl_destroy(void* comm) {
+  PB_NCCL(ncclCommDestroy((ncclComm_t)comm));
+  return PB_OK;
+}
+
+int pb_nccl_allreduce(void* comm, uint64_t send, uint64_t recv, uint64_t count, int dtype, int op) {
+  int rc = fence_compute_to_comm();
+  if (rc) return rc;
+  ncclRedOp_t o = op == 1 ? ncclMax : (op == 2 ? ncclAvg : ncclSum);
+  PB_NCCL(ncclAllReduce((const void*)(uintptr_t)send, (void*)(uintptr_t)recv, count, nccl_type(dtype), o,
+                        (ncclComm_t)comm, comm_stream()));
+  return PB_OK;
+}
+
+int pb_nccl_broadcast(void* comm, uint64_t send, uint64_t recv, uint64_t count, int dtype, int root) {
+  int rc = fence_compute_to_comm();
+  if (rc) return rc;
+  PB_NCCL(ncclBroadcast((const void*)(uintptr_t)send, (void*)(uintptr_t)recv, count, nccl_type(dtype), root,
+                        (ncclComm_t)comm, comm_stream()));
+  return PB_OK;
+}
+
+int pb_nccl_allgather(void* comm, uint64_t send, uint64_t recv, uint64_t count, int dtype) {
+  int rc = fence_compute_to_comm();
+  if (rc) return rc;
+  PB_NCCL(ncclAllGather((const void*)(uintptr_t)send, (void*)(uintptr_t)recv, count, nccl_type(dtype),
+                        (ncclComm_t)comm, comm_stream()));
+  return PB_OK;
+}
+
+int pb_nccl_wait(void* comm) {
+  (void)comm;
+  cudaEvent_t ev;
+  PB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  PB_CUDA(cudaEventRecord(ev, comm_stream()));
+  PB_CUDA(cudaStreamWaitEvent(compute_stream(), ev, 0));
+  PB_CUDA(cudaEventDestroy(ev));
+  return PB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,499 @@
+"""GpuBackend: the B200 implementation of the reference's Backend contract.
+
+``execute(call, args)`` (minml/registry.py:137-138) runs each of the 41 primitives as a
+CUDA kernel from libpaper_b200.so on the backend's compute stream, with one allocation
+per op from the stream-ordered caching allocator (the template of minml/eager.py:33-53).
+
+Adapters are ``DeviceArray`` views (pointer, shape, element strides) over refcounted
+``DevBlock`` allocations.  Because tensors are immutable, movement primitives are free:
+``reshape`` of a contiguous tensor, ``transpose`` and ``slice`` return views, and
+``full`` is a single element with all-zero strides (the sum-backward ``ones`` spreads
+of minml/autograd.py:615-617 cost no HBM traffic).  Consumers read views through
+strides; only contiguous-only kernels (conv, full reductions, transfers) materialise.
+
+Nothing here falls back to the host: if the extension or a device is missing, the
+backend cannot be constructed.
+"""
+
+import ctypes
+import sys
+
+import numpy as np
+
+from .. import dtypes
+from ..errors import DomainError, DTypeError
+from ..memory import CachingManager, MemoryManager, op_tag
+from ..registry import Backend
+from ..shape import normalize_axis
+from . import _lib
+
+_pack = _lib.pack_tensor
+_CONTIG = {}
+
+
+def contig_strides(shape):
+    s = _CONTIG.get(shape)
+    if s is None:
+        acc, out = 1, []
+        for d in reversed(shape):
+            out.append(acc)
+            acc *= d
+        s = _CONTIG[shape] = tuple(reversed(out))
+    return s
+
+
+def device_available():
+    lib = _lib.load()
+    return lib.pb_device_count() > 0
+
+
+class DevBlock:
+    """One allocation; returned to the allocator (stream-ordered) when the last view dies."""
+
+    __slots__ = ("mm", "id", "ptr", "ledger", "__weakref__")
+
+    def __init__(self, mm, bid, ptr, ledger=None):
+        self.mm = mm
+        self.id = bid
+        self.ptr = ptr
+        self.ledger = ledger
+
+    def __del__(self):
+        lib = _lib._lib
+        if lib is not None:
+            lib.pb_mm_free(self.mm, self.id)
+            if self.ledger is not None:
+                mgr, blk = self.ledger
+                try:
+                    mgr.free(blk)
+                except Exception:
+                    pass
+
+
+class DeviceArray:
+    """Adapter: a strided view (element strides) into a DevBlock."""
+
+    __slots__ = ("block", "ptr", "shape", "strides", "dtype", "host", "__weakref__")
+
+    def __init__(self, block, ptr, shape, strides, dtype, host=None):
+        self.block = block
+        self.ptr = ptr
+        self.shape = shape
+        self.strides = strides
+        self.dtype = dtype
+        self.host = host
+
+    def packed(self):
+        return _pack(self.ptr, self.dtype.code, self.shape, self.strides)
+
+    @property
+    def contiguous(self):
+        if self.strides == contig_strides(self.shape):
+            return True
+        exp = 1
+        for d, s in zip(reversed(self.shape), reversed(self.strides)):
+            if d != 1 and s != exp:
+                return False
+            exp *= d
+        return True
+
+
+_LOGICAL = ("logical_and", "logical_or")
+_CT = {}
+
+
+def compute_dtype(name, da, other, scalar):
+    """numpy's result type for the op (NEP 50 weak scalars); true division of ints -> f64."""
+    key = (name, da, type(other) if scalar else other)
+    ct = _CT.get(key)
+    if ct is None:
+        if name in _LOGICAL:
+            ct = dtypes.bool_
+        else:
+            rt = np.result_type(da.np, other) if scalar else np.result_type(da.np, other.np)
+            ct = dtypes.from_numpy(rt)
+            if name == "div" and not ct.is_float:
+                ct = dtypes.f64
+        _CT[key] = ct
+    return ct
+
+
+_INT_RANGE = {"u8": (0, 255), "i32": (-2**31, 2**31 - 1), "i64": (-2**63, 2**63 - 1)}
+
+
+class GpuBackend(Backend):
+    def __init__(self, name="gpu", seed=0, device=0):
+        self._lib = _lib.load()
+        _lib.check(self._lib.pb_init(device), "pb_init")
+        self.device = device
+        super().__init__(name, seed)
+        self._blk = _lib.MMBlock()
+        self._blk_ref = ctypes.byref(self._blk)
+        self._flag = ctypes.c_int32(0)
+        self._ops = {
+            "full": self._full, "arange": self._arange, "rand_uniform": self._rand, "rand_normal": self._rand,
+            "from_host": self._from_host, "to_host": self._to_host, "matmul": self._matmul,
+            "conv2d": self._conv2d, "conv2d_grad_input": self._conv_gi, "conv2d_grad_weight": self._conv_gw,
+            "reshape": self._reshape, "transpose": self._transpose, "concat": self._concat, "slice": self._slice,
+            "pad": self._pad, "sum": self._reduce, "max_reduce": self._reduce, "min_reduce": self._reduce,
+            "argmax": self._reduce, "astype": self._unary,
+        }
+        for n in _lib.BINOP:
+            self._ops[n] = self._binary
+        for n in _lib.UNOP:
+            self._ops[n] = self._unary
+
+    # ------------------------------------------------------------------ memory
+    def _default_manager(self):
+        return CachingManager()
+
+    def _bind_manager(self):
+        m = self._manager
+        if isinstance(m, MemoryManager) and not m.simulate:
+            return m.handle, None
+        # a foreign (e.g. reference-side) manager keeps the ledger; device memory comes
+        # from a private caching allocator so its alloc/free/stats stay exact
+        if not hasattr(self, "_private"):
+            self._private = CachingManager()
+        return self._private.handle, m
+
+    @property
+    def manager(self):
+        return self._manager
+
+    def attach_manager(self, manager):
+        super().attach_manager(manager)
+        self._mm = self._bind_manager()
+
+    def detach_manager(self):
+        old = super().detach_manager()
+        self._mm = self._bind_manager()
+        return old
+
+    def _alloc(self, nbytes, opname):
+        try:
+            h, ledger = self._mm
+        except AttributeError:
+            self._mm = self._bind_manager()
+            h, ledger = self._mm
+        rc = self._lib.pb_mm_alloc(h, nbytes, op_tag(opname), self._blk_ref)
+        if rc:
+            _lib.check(rc, f"alloc {nbytes} B for {opname}")
+        b = self._blk
+        led = None
+        if ledger is not None:
+            led = (ledger, ledger.alloc(nbytes, op=opname))
+        return DevBlock(h, b.id, b.ptr, led)
+
+    def _new(self, shape, dt, opname):
+        n = 1
+        for d in shape:
+            n *= d
+        nbytes = n * dt.itemsize
+        if nbytes == 0:
+            return DeviceArray(None, 0, shape, contig_strides(shape), dt)
+        blk = self._alloc(nbytes, opname)
+        return DeviceArray(blk, blk.ptr, shape, contig_strides(shape), dt)
+
+    def _contig(self, a, opname="materialize"):
+        if a.contiguous:
+            return a
+        out = self._new(a.shape, a.dtype, opname)
+        if out.block is not None:
+            _lib.check(self._lib.pb_copy(a.packed(), out.packed()), "materialize")
+        return out
+
+    # ----------------------------------------------------------------- execute
+    def execute(self, call, args):
+        ledger = self._manager if not isinstance(self._manager, MemoryManager) else None
+        if ledger is not None:
+            ledger.on_op_begin(call.name)
+            try:
+                return self._ops[call.name](call, args)
+            finally:
+                ledger.on_op_end(call.name)
+        return self._ops[call.name](call, args)
+
+    def synchronize(self):
+        _lib.check(self._lib.pb_synchronize(), "synchronize")
+
+    # creation / transfer
+    def _full(self, call, args):
+        shape = tuple(call.shape)
+        dt = call.dtype
+        if call.shape.size == 0:
+            return DeviceArray(None, 0, shape, contig_strides(shape), dt)
+        blk = self._alloc(dt.itemsize, "full")
+        one = DeviceArray(blk, blk.ptr, (1,), (1,), dt)
+        _lib.check(self._lib.pb_fill(one.packed(), _lib.pack_scalar(call.params["value"])), "full")
+        return DeviceArray(blk, blk.ptr, shape, (0,) * len(shape), dt)
+
+    def _arange(self, call, args):
+        out = self._new(tuple(call.shape), call.dtype, "arange")
+        if out.block is not None:
+            _lib.check(self._lib.pb_arange(out.packed()), "arange")
+        return out
+
+    def _rand(self, call, args):
+        out = self._new(tuple(call.shape), call.dtype, call.name)
+        if out.block is not None:
+            p = call.params
+            _lib.check(self._lib.pb_rand(1 if call.name == "rand_normal" else 0, p["seed"] & ((1 << 64) - 1),
+                                         p["offset"], out.packed()), call.name)
+        return out
+
+    def _from_host(self, call, args):
+        host = np.ascontiguousarray(call.params["array"])
+        out = self._new(tuple(call.shape), call.dtype, "from_host")
+        if out.block is not None:
+            _lib.check(self._lib.pb_h2d(out.ptr, host.ctypes.data, host.nbytes), "from_host")
+            # integer operands (labels, token ids) keep a host mirror: cross_entropy's range
+            # check (minml/nn.py:373) then reads it without a device round trip
+            if host.dtype.kind in "iu" and host.size <= (1 << 20):
+                out.host = host.copy()
+        return out
+
+    def _to_host(self, call, args):
+        a = args[0]
+        if a.host is not None:
+            return a.host.copy()
+        res = np.empty(a.shape, dtype=a.dtype.np)
+        if res.size == 0:
+            return res
+        a = self._contig(a)
+        _lib.check(self._lib.pb_d2h(res.ctypes.data, a.ptr, res.nbytes), "to_host")
+        return res
+
+    # elementwise
+    def _binary(self, call, args):
+        name = call.name
+        p = call.params
+        out = self._new(tuple(call.shape), call.dtype, name)
+        if out.block is None:
+            return out
+        if "scalar" in p:
+            s = p["scalar"]
+            a = args[0]
+            ct = compute_dtype(name, a.dtype, s, True)
+            if type(s) is int and ct.kind in "iu":
+                lo, hi = _INT_RANGE[ct.name]
+                if not lo <= s <= hi:
+                    raise OverflowError(f"Python integer {s} out of bounds for {ct.np}")
+            left = p.get("scalar_side") == "left"
+            if name == "div" and ct.is_float:
+                if not left and type(s) is int and a.dtype.is_integer and s == 0:
+                    raise DomainError("integer division by zero")
+                if left and type(s) is int and a.dtype.is_integer:
+                    self._domain_check(0, a, "integer division by zero")
+            if name == "pow" and ct.is_integer:
+                if (not left and type(s) is int and s < 0) or left:
+                    if not left or self._any(1, a):
+                        raise DomainError("Integers to negative integer powers are not allowed.")
+            pa = a.packed()
+            rc = self._lib.pb_binary(_lib.BINOP[name], None if left else pa, pa if left else None,
+                                     _lib.pack_scalar(s), ct.code, out.packed())
+        else:
+            a, b = args
+            ct = compute_dtype(name, a.dtype, b.dtype, False)
+            if name == "div" and a.dtype.is_integer and b.dtype.is_integer:
+                self._domain_check(0, b, "integer division by zero")
+            if name == "pow" and ct.is_integer and self._any(1, b):
+                raise DomainError("Integers to negative integer powers are not allowed.")
+            rc = self._lib.pb_binary(_lib.BINOP[name], a.packed(), b.packed(), None, ct.code, out.packed())
+        if rc:
+            _lib.check(rc, name)
+        return out
+
+    def _any(self, what, a):
+        _lib.check(self._lib.pb_check(what, a.packed(), ctypes.byref(self._flag)), "check")
+        return self._flag.value != 0
+
+    def _domain_check(self, what, a, msg):
+        if self._any(what, a):
+            raise DomainError(msg)
+
+    def _unary(self, call, args):
+        a = args[0]
+        out = self._new(tuple(call.shape), call.dtype, call.name)
+        if out.block is None:
+            return out
+        ct = call.dtype if call.name == "astype" else a.dtype
+        _lib.check(self._lib.pb_unary(_lib.UNOP[call.name], a.packed(), ct.code, out.packed()), call.name)
+        return out
+
+    # reductions
+    def _reduce(self, call, args):
+        a = args[0]
+        out = self._new(tuple(call.shape), call.dtype, call.name)
+        if out.block is None:
+            return out
+        axis = call.params.get("axis")
+        if axis is None:
+            a = self._contig(a)
+            ax = -1
+        else:
+            ax = normalize_axis(axis, len(a.shape))
+        _lib.check(self._lib.pb_reduce(_lib.REDOP[call.name], a.packed(), ax, out.packed()), call.name)
+        return out
+
+    # contractions
+    def _matmul(self, call, args):
+        a, b = args
+        out = self._new(tuple(call.shape), call.dtype, "matmul")
+        if out.block is None:
+            return out
+        _lib.check(self._lib.pb_matmul(a.packed(), b.packed(), out.packed()), "matmul")
+        return out
+
+    def _conv_params(self, call):
+        (sh, sw), (ph, pw) = call.params["stride"], call.params["padding"]
+        return _lib.CONV.pack(sh, sw, ph, pw)
+
+    def _conv2d(self, call, args):
+        x, w = self._contig(args[0]), self._contig(args[1])
+        bias = self._contig(args[2]).packed() if len(args) == 3 else None
+        out = self._new(tuple(call.shape), call.dtype, "conv2d")
+        if out.block is None:
+            return out
+        _lib.check(self._lib.pb_conv2d(x.packed(), w.packed(), bias, self._conv_params(call), out.packed()),
+                   "conv2d")
+        return out
+
+    def _conv_gi(self, call, args):
+        g, w = self._contig(args[0]), self._contig(args[1])
+        out = self._new(tuple(call.shape), call.dtype, "conv2d_grad_input")
+        if out.block is None:
+            return out
+        _lib.check(self._lib.pb_conv2d_grad_input(g.packed(), w.packed(), self._conv_params(call), out.packed()),
+                   "conv2d_grad_input")
+        return out
+
+    def _conv_gw(self, call, args):
+        x, g = self._contig(args[0]), self._contig(args[1])
+        out = self._new(tuple(call.shape), call.dtype, "conv2d_grad_weight")
+        if out.block is None:
+            return out
+        _lib.check(self._lib.pb_conv2d_grad_weight(x.packed(), g.packed(), self._conv_params(call), out.packed()),
+                   "conv2d_grad_weight")
+        return out
+
+    # movement: views where possible
+    def _reshape(self, call, args):
+        a = args[0]
+        shape = tuple(call.shape)
+        if not a.contiguous:
+            a = self._contig(a, "reshape")
+        return DeviceArray(a.block, a.ptr, shape, contig_strides(shape), a.dtype, a.host.reshape(shape)
+                           if a.host is not None else None)
+
+    def _transpose(self, call, args):
+        a = args[0]
+        perm = call.params.get("perm") or tuple(range(len(a.shape) - 1, -1, -1))
+        return DeviceArray(a.block, a.ptr, tuple(a.shape[i] for i in perm), tuple(a.strides[i] for i in perm),
+                           a.dtype)
+
+    def _slice(self, call, args):
+        a = args[0]
+        p = call.params
+        off = 0
+        for st, s in zip(p["starts"], a.strides):
+            off += st * s
+        strides = tuple(s * k for s, k in zip(a.strides, p["steps"]))
+        shape = tuple(call.shape)
+        if 0 in shape:
+            return DeviceArray(None, 0, shape, contig_strides(shape), a.dtype)
+        return DeviceArray(a.block, a.ptr + off * a.dtype.itemsize, shape, strides, a.dtype)
+
+    def _concat(self, call, args):
+        out = self._new(tuple(call.shape), call.dtype, "concat")
+        if out.block is None:
+            return out
+        ax = normalize_axis(call.params["axis"], len(out.shape))
+        off = 0
+        for a in args:
+            e = a.shape[ax]
+            if e:
+                dst = DeviceArray(out.block, out.ptr + off * out.strides[ax] * out.dtype.itemsize,
+                                  a.shape, out.strides, out.dtype)
+                _lib.check(self._lib.pb_copy(a.packed(), dst.packed()), "concat")
+            off += e
+        return out
+
+    def _pad(self, call, args):
+        a = args[0]
+        out = self._new(tuple(call.shape), call.dtype, "pad")
+        if out.block is None:
+            return out
+        lo = (ctypes.c_int64 * 8)(*[lo for lo, _ in call.params["pad_width"]])
+        _lib.check(self._lib.pb_pad(a.packed(), lo, _lib.pack_scalar(call.params.get("value", 0)), out.packed()),
+                   "pad")
+        return out
+
+    # ---------------------------------------------------------- fused optimizer
+    def fused_sgd(self, params, velocity, lr, momentum, weight_decay):
+        """SGD.step for every parameter in one launch (same op order as minml/optim.py:64-72).
+
+        Updates in place when the parameter / velocity buffer is exclusively owned
+        (nothing else references the tensor or its storage), otherwise writes fresh
+        buffers and rebinds ``p.data`` exactly like the reference.
+        """
+        f32 = dtypes.f32
+        from .._tensor import Tensor
+        n = len(params)
+        pin = (ctypes.c_uint64 * n)()
+        pout = (ctypes.c_uint64 * n)()
+        gs = (ctypes.c_uint64 * n)()
+        vin = (ctypes.c_uint64 * n)() if velocity is not None else None
+        vout = (ctypes.c_uint64 * n)() if velocity is not None else None
+        numel = (ctypes.c_int64 * n)()
+        rebind_p, rebind_v, keep = [], [], []
+        for i, p in enumerate(params):
+            t = p.data
+            g = p.grad
+            if t.dtype is not f32 or g.dtype is not f32 or t.backend_id != self.name:
+                return False
+            arr = t.adapter
+            garr = self._contig(g.adapter)
+            keep.append(garr)
+            numel[i] = t.shape.size
+            gs[i] = garr.ptr
+            pin[i] = arr.ptr
+            if _exclusive(t, arr):
+                pout[i] = arr.ptr
+            else:
+                na = self._new(arr.shape, f32, "sgd")
+                pout[i] = na.ptr
+                rebind_p.append((p, na))
+            if velocity is not None:
+                vt = velocity[i]
+                va = vt.adapter
+                vin[i] = va.ptr
+                if _exclusive(vt, va):
+                    vout[i] = va.ptr
+                else:
+                    nv = self._new(va.shape, f32, "sgd")
+                    vout[i] = nv.ptr
+                    rebind_v.append((i, nv))
+                    if not va.contiguous:  # stride-0 zeros: read through a dense copy
+                        dv = self._contig(va)
+                        keep.append(dv)
+                        vin[i] = dv.ptr
+            if not arr.contiguous:
+                da = self._contig(arr)
+                keep.append(da)
+                pin[i] = da.ptr
+        _lib.check(self._lib.pb_sgd(n, pin, pout, gs, vin, vout, numel, lr, momentum, weight_decay), "sgd")
+        self.last_sgd = {"params": n, "rebound": len(rebind_p), "velocity_rebound": len(rebind_v)}
+        for p, na in rebind_p:
+            p.data = Tensor(na, self.name, p.data.shape, f32)
+        for i, nv in rebind_v:
+            velocity[i] = Tensor(nv, self.name, velocity[i].shape, f32)
+        return True
+
+
+def _exclusive(t, arr):
+    """True when only the owner references tensor ``t``, its adapter and its storage."""
+    if not arr.contiguous or arr.block is None or arr.ptr != arr.block.ptr:
+        return False
+    # references: the owner's attribute + getrefcount's argument + our local name(s)
+    return sys.getrefcount(t) <= 4 and sys.getrefcount(arr) <= 4 and sys.getrefcount(arr.block) <= 2
