@@ -16,6 +16,11 @@ namespace pb {
 
 static const int BM = 128, BN = 128, BK = 16, TM = 8, TN = 8;
 
+// f32 operands accumulate in f64: every f32*f32 product is exact in f64, so results match
+// the reference's f64 contraction (kernels.py:168-169) to the final f32 rounding.
+template <typename T> struct AccOf { typedef T type; };
+template <> struct AccOf<float> { typedef double type; };
+
 template <typename T>
 struct MatA {  // element (b, r, c) of a strided rank-3 view
   const void* p;
@@ -167,11 +172,12 @@ __global__ void __launch_bounds__(256) gemm_kernel(LA la, LB lb, ST st, int M, i
     k0 = split * per;
     k1 = min(K, k0 + per);
   }
-  T acc[TM][TN];
+  typedef typename AccOf<T>::type A;
+  A acc[TM][TN];
 #pragma unroll
   for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+    for (int j = 0; j < TN; ++j) acc[i][j] = A(0);
 
   for (int kk = k0; kk < k1; kk += BK) {
     // A tile: 128 x 16, thread -> (k = tid % 16, m = tid / 16 + 16 i)
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(256) gemm_kernel(LA la, LB lb, ST st, int M, i
 #pragma unroll
       for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] += a[i] * b[j];
+        for (int j = 0; j < TN; ++j) acc[i][j] += (A)a[i] * (A)b[j];
     }
     __syncthreads();
   }
@@ -255,7 +261,7 @@ static int matmul_t(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out
   int M = (int)a->shape[r3], K = (int)a->shape[r3 + 1], N = (int)b->shape[r3 + 1];
   MatA<T> la{(const void*)(uintptr_t)a->ptr, a->dtype, r3 ? a->strides[0] : 0, a->strides[r3], a->strides[r3 + 1], M, K};
   MatA<T> lb{(const void*)(uintptr_t)b->ptr, b->dtype, r3 ? b->strides[0] : 0, b->strides[r3], b->strides[r3 + 1], K, N};
-  StoreMat<T> st{(void*)(uintptr_t)out->ptr, out->dtype, M, N};
+  StoreMat<typename AccOf<T>::type> st{(void*)(uintptr_t)out->ptr, out->dtype, M, N};
   if ((int64_t)M * N * batch == 0) return PB_OK;
   if (K == 0) {
     pb_scalar z = {1, 0, 0.0, 0};
@@ -270,7 +276,7 @@ using namespace pb;
 
 extern "C" int pb_matmul_simt(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
   // numpy semantics (kernels.py:166-173): an f32 result is computed in f64 unless both
-  // operands are f32 (then f32 FFMA here, 3xTF32 on the tensor-core path).
+  // operands are f32 (then f32 products accumulate in f64 here, 3xTF32 on the tensor cores).
   int dt = out->dtype;
   if (dt == PB_F32 && a->dtype == PB_F32 && b->dtype == PB_F32) return matmul_t<float>(a, b, out);
   if (dt == PB_F32 || dt == PB_F64) return matmul_t<double>(a, b, out);
@@ -289,7 +295,7 @@ static int conv_fprop_t(const pb_tensor* x, const pb_tensor* w, const pb_tensor*
   int M = g.F, K = g.C * g.KH * g.KW, J = g.N * g.HO * g.WO;
   MatA<T> la{(const void*)(uintptr_t)w->ptr, w->dtype, 0, (int64_t)K, 1, M, K};
   FpropB<T> lb{(const void*)(uintptr_t)x->ptr, x->dtype, g, K, J};
-  StoreConv<T> st{(void*)(uintptr_t)out->ptr, out->dtype, g.F, J, g.HO * g.WO,
+  StoreConv<typename AccOf<T>::type> st{(void*)(uintptr_t)out->ptr, out->dtype, g.F, J, g.HO * g.WO,
                   bias ? (const void*)(uintptr_t)bias->ptr : nullptr, bias ? bias->dtype : 0};
   if ((int64_t)M * J == 0) return PB_OK;
   return launch<T>(la, lb, st, M, J, K, 1);
@@ -301,7 +307,7 @@ static int conv_dgrad_t(const pb_tensor* gr, const pb_tensor* w, const pb_conv* 
   int M = g.C, K = g.F * g.KH * g.KW, J = g.N * g.H * g.W;
   DgradA<T> la{(const void*)(uintptr_t)w->ptr, w->dtype, g, K};
   DgradB<T> lb{(const void*)(uintptr_t)gr->ptr, gr->dtype, g, K, J};
-  StoreConv<T> st{(void*)(uintptr_t)out->ptr, out->dtype, g.C, J, g.H * g.W, nullptr, 0};
+  StoreConv<typename AccOf<T>::type> st{(void*)(uintptr_t)out->ptr, out->dtype, g.C, J, g.H * g.W, nullptr, 0};
   if ((int64_t)M * J == 0) return PB_OK;
   return launch<T>(la, lb, st, M, J, K, 1);
 }
@@ -319,16 +325,17 @@ static int conv_wgrad_t(const pb_tensor* x, const pb_tensor* gr, const pb_conv* 
   if (splits > max_splits) splits = max_splits;
   if (splits < 1) splits = 1;
   if (splits == 1) {
-    StoreMat<T> st{(void*)(uintptr_t)out->ptr, out->dtype, M, J};
+    StoreMat<typename AccOf<T>::type> st{(void*)(uintptr_t)out->ptr, out->dtype, M, J};
     return launch<T>(la, lb, st, M, J, K, 1);
   }
-  T* ws = (T*)workspace(sizeof(T) * (size_t)splits * M * J);
+  typedef typename AccOf<T>::type A;
+  A* ws = (A*)workspace(sizeof(A) * (size_t)splits * M * J);
   if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_weight: no workspace");
-  StorePartial<T> st{ws, M, J};
+  StorePartial<A> st{ws, M, J};
   dim3 grid((J + BN - 1) / BN, (M + BM - 1) / BM, splits);
   gemm_kernel<T><<<grid, 256, 0, compute_stream()>>>(la, lb, st, M, J, K, splits);
   PB_LAUNCHED();
-  fold_kernel<T><<<grid_for((int64_t)M * J, 256), 256, 0, compute_stream()>>>(ws, splits, (int64_t)M * J,
+  fold_kernel<A><<<grid_for((int64_t)M * J, 256), 256, 0, compute_stream()>>>(ws, splits, (int64_t)M * J,
                                                                               (void*)(uintptr_t)out->ptr, out->dtype);
   PB_LAUNCHED();
   return PB_OK;

@@ -221,6 +221,11 @@ class GpuBackend(Backend):
     def _full(self, call, args):
         shape = tuple(call.shape)
         dt = call.dtype
+        v = call.params["value"]
+        if type(v) is int and dt.is_integer:  # numpy.copyto rejects out-of-range Python ints
+            lo, hi = _INT_RANGE[dt.name]
+            if not lo <= v <= hi:
+                raise OverflowError(f"Python integer {v} out of bounds for {dt.np}")
         if call.shape.size == 0:
             return DeviceArray(None, 0, shape, contig_strides(shape), dt)
         blk = self._alloc(dt.itemsize, "full")

@@ -25,8 +25,9 @@ def test_trajectory_matches_reference(name):
     be = gpu_backend()
     meta = META[name]
     losses, sums, _ = run_trajectory(name, meta, be)
-    # north-star tolerance: loss trajectories within 1e-3; we hold them much tighter
-    assert rel_err(losses, meta["losses"]) <= 1e-4, (losses, meta["losses"])
+    # north-star tolerance (BASELINE.json): loss trajectories within 1e-3.  The tiny
+    # BatchNorm nets (batch 4) amplify f32-vs-f64 contraction rounding the most.
+    assert rel_err(losses, meta["losses"]) <= 1e-3, (losses, meta["losses"])
     assert rel_err(sums, meta["param_sums"]) <= 1e-3
 
 
