@@ -17,7 +17,10 @@ if os.environ.get("PB_NO_AUTOREGISTER") != "1":
         from .gpu.backend import GpuBackend, device_available
 
         if device_available():
-            registry.register(GpuBackend("gpu"))
+            from .gpu import _lib as _l
+
+            _ndev = _l.load().pb_device_count()
+            registry.register(GpuBackend("gpu", device=int(os.environ.get("LOCAL_RANK", "0")) % _ndev))
         else:
             registry._load_error = "no CUDA device visible"
     except (OSError, ImportError) as exc:  # libpaper_b200.so missing or unloadable

@@ -217,6 +217,24 @@ class GpuBackend(Backend):
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
 
+    def launch_count(self):
+        """Kernels this library has launched so far (all backends in the process)."""
+        return int(self._lib.pb_launch_count())
+
+    def event_timer(self):
+        """CUDA-event timer on the compute stream: ``t = be.event_timer(); ...; ms = t()``."""
+        h = ctypes.c_uint64(0)
+        ms = ctypes.c_float(0)
+        _lib.check(self._lib.pb_timer(0, ctypes.byref(h), ctypes.byref(ms)), "timer")
+
+        def stop():
+            _lib.check(self._lib.pb_timer(1, ctypes.byref(h), ctypes.byref(ms)), "timer")
+            _lib.check(self._lib.pb_timer(2, ctypes.byref(h), ctypes.byref(ms)), "timer")
+            self._lib.pb_timer(3, ctypes.byref(h), ctypes.byref(ms))
+            return float(ms.value)
+
+        return stop
+
     # creation / transfer
     def _full(self, call, args):
         shape = tuple(call.shape)
@@ -433,6 +451,60 @@ class GpuBackend(Backend):
         _lib.check(self._lib.pb_pad(a.packed(), lo, _lib.pack_scalar(call.params.get("value", 0)), out.packed()),
                    "pad")
         return out
+
+    # -------------------------------------------------------------- collectives
+    def _tensor(self, arr, shape):
+        from .._tensor import Tensor
+        return Tensor(arr, self.name, shape, arr.dtype)
+
+    def bucket_pack(self, grads):
+        """Concatenate flattened f32 gradients into one bucket with a single launch."""
+        n = len(grads)
+        srcs = (ctypes.c_uint64 * n)()
+        numel = (ctypes.c_int64 * n)()
+        keep, total = [], 0
+        for i, g in enumerate(grads):
+            a = self._contig(g.adapter)
+            keep.append(a)
+            srcs[i] = a.ptr
+            numel[i] = g.shape.size
+            total += g.shape.size
+        out = self._new((total,), dtypes.f32, "bucket")
+        _lib.check(self._lib.pb_bucket_pack(n, srcs, numel, out.ptr), "bucket_pack")
+        return self._tensor(out, (total,))
+
+    def nccl_all_reduce(self, comm, tensor, op="sum", wait=True):
+        a = self._contig(tensor.adapter)
+        out = self._new(a.shape, a.dtype, "all_reduce")
+        _lib.check(self._lib.pb_nccl_allreduce(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code,
+                                               0 if op == "sum" else 1), "ncclAllReduce")
+        if wait:
+            self.nccl_wait(comm)
+        else:
+            out.host = None
+            self._inflight = getattr(self, "_inflight", [])
+            self._inflight.append(a)  # source must outlive the collective
+        return self._tensor(out, tuple(tensor.shape))
+
+    def nccl_wait(self, comm):
+        _lib.check(self._lib.pb_nccl_wait(comm), "nccl wait")
+        self._inflight = []
+
+    def nccl_all_gather(self, comm, tensor, world):
+        a = self._contig(tensor.adapter)
+        out = self._new((world,) + a.shape, a.dtype, "all_gather")
+        _lib.check(self._lib.pb_nccl_allgather(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code),
+                   "ncclAllGather")
+        self.nccl_wait(comm)
+        return self._tensor(out, (world,) + tuple(tensor.shape))
+
+    def nccl_broadcast(self, comm, tensor, root):
+        a = self._contig(tensor.adapter)
+        out = self._new(a.shape, a.dtype, "broadcast")
+        _lib.check(self._lib.pb_nccl_broadcast(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code, root),
+                   "ncclBroadcast")
+        self.nccl_wait(comm)
+        return self._tensor(out, tuple(tensor.shape))
 
     # ---------------------------------------------------------- fused optimizer
     def fused_sgd(self, params, velocity, lr, momentum, weight_decay):

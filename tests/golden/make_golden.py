@@ -330,9 +330,9 @@ def build_models():
     meta["bert_tiny"] = dict(m, vocab=vocab, seq=seq, batch=4)
     # data parallel: 2 thread ranks x 8 vs the reference's own run_ranks
     world, per, steps = 2, 8, 5
-    ds = MD.synth_blobs(64, seed=21, dim=784)
-    bx = np.stack([ds[i][0] for i in range(world * per * 2)])
-    by = np.array([ds[i][1] for i in range(world * per * 2)], np.int64)
+    b0, b1 = GI.batch("dp_mlp", 0, (784,), 10, world * per), GI.batch("dp_mlp", 1, (784,), 10, world * per)
+    bx = np.concatenate([b0[0], b1[0]])
+    by = np.concatenate([b0[1], b1[1]])
     for r in range(world):
         MR.register(EagerBackend(name=f"gold-dp-{r}", seed=13))
 
