@@ -209,11 +209,11 @@ def main():
         t = comm.all_reduce(T.tensor(np.array([v], np.float64), backend=be.name), "max")
         return float(t.numpy()[0])
 
-    # ---- device-resident steps (value)
+    # ---- eager front end (one Python dispatch per primitive): reported beside the graph
     xd = Variable(T.tensor(x_host, backend=be.name))
     yd = T.tensor(y_host, backend=be.name)
 
-    def resident_step():
+    def eager_step():
         opt.zero_grad()
         loss = nn.cross_entropy(model(xd), yd)
         if ddp is not None:
@@ -223,36 +223,65 @@ def main():
         opt.step()
         return loss
 
-    for _ in range(args.warmup):
-        resident_step()
+    for _ in range(2):
+        eager_step()
     barrier()
     l0 = be.launch_count()
+    n_eager = 3
+    t0 = time.perf_counter()
+    stop = be.event_timer()
+    for _ in range(n_eager):
+        eager_step()
+    eager_ms = max_over_ranks(stop()) / n_eager
+    eager_wall = (time.perf_counter() - t0) * 1e3 / n_eager
+    eager_launches = (be.launch_count() - l0) // n_eager
+
+    # ---- whole-step CUDA graph (training.CapturedStep): device-resident replays (value)
+    step = training.CapturedStep(model, opt, ddp=ddp, warmup=1)
+    graph_error = None
+    try:
+        for _ in range(1 + max(args.warmup, 3)):
+            step(x_host, y_host)
+    except Exception as e:  # noqa: BLE001 -- report, then measure the eager path instead
+        graph_error = f"{type(e).__name__}: {e}"
+        step = None
+    barrier()
     with Clocks(local) as clk:
         stop = be.event_timer()
         for _ in range(args.steps):
-            loss = resident_step()
+            if step is not None:
+                step.graph.launch()
+            else:
+                eager_step()
         ms_total = stop()
         barrier()
-    launches = (be.launch_count() - l0) // args.steps
+    launches = step.launches if step is not None else eager_launches
     ms_total = max_over_ranks(ms_total)
     ms_step = ms_total / args.steps
     value = world * BATCH * args.steps / (ms_total / 1e3)
-    final_loss = float(loss.scalar())
+    final_loss = float(step.loss.scalar()) if step is not None else float(eager_step().scalar())
 
-    # ---- end to end through the public API with host buffers (e2e)
+    # ---- end to end through the public API with host buffers (e2e): H2D + replay + loss D2H
+    run = step if step is not None else (lambda xh, yh: training.train_step(model, xh, yh, opt, ddp=ddp))
     for _ in range(2):
-        training.train_step(model, x_host, y_host, opt, ddp=ddp)
+        run(x_host, y_host)
     barrier()
     t0 = time.perf_counter()
     stop = be.event_timer()
     for _ in range(args.steps):
-        training.train_step(model, x_host, y_host, opt, ddp=ddp)
+        run(x_host, y_host)
     e2e_ms = stop()
     wall = time.perf_counter() - t0
     e2e_ms = max_over_ranks(e2e_ms)
     e2e = {"value": world * BATCH * args.steps / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(x_host.nbytes + y_host.nbytes), "d2h_bytes_per_step": 4,
-           "ms_per_step": e2e_ms / args.steps, "host_wall_ms_per_step": wall * 1e3 / args.steps}
+           "ms_per_step": e2e_ms / args.steps, "host_wall_ms_per_step": wall * 1e3 / args.steps,
+           "api": "training.CapturedStep(model, opt)(images, labels)" if step is not None else
+                  "training.train_step(model, images, labels, opt)"}
+    eager = {"value": world * BATCH / (eager_ms / 1e3), "unit": UNIT, "ms_per_step": eager_ms,
+             "host_wall_ms_per_step": eager_wall, "launches_per_step": eager_launches,
+             "host_us_per_launch": eager_wall * 1e3 / max(eager_launches, 1),
+             "note": "train_step semantics, one Python dispatch per primitive, no graph"}
 
     if rank != 0:
         return
@@ -267,7 +296,10 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) images)",
             "config": cfg, "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
             "roofline": roofline, "clocks": clk.summary(), "final_loss": final_loss,
-            "gemm_path": "tcgen05" if be._lib.pb_gemm_path() else "simt"}
+            "gemm_path": "tcgen05" if be._lib.pb_gemm_path() else "simt",
+            "step_mode": "cuda_graph" if step is not None else "eager", "eager": eager}
+    if graph_error:
+        line["graph_error"] = graph_error
     if world == 1 and not args.no_cpu_baseline:
         v, ms = cpu_reference(2, 1)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",

@@ -270,6 +270,8 @@ class Manager {
   uint64_t flush_all(bool everything) {
     uint64_t released = 0;
     for (auto& pc : caches_) {
+      // private pools hold addresses recorded into CUDA graphs: only the destructor frees them
+      if (pc.first != 0 && !everything) continue;
       for (auto& kv : pc.second) {
         for (auto& e : kv.second) {
           ++released;
@@ -280,7 +282,6 @@ class Manager {
       pc.second.clear();
     }
     free_count_ += released;
-    (void)everything;
     return released;
   }
 

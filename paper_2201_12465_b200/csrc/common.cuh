@@ -136,6 +136,22 @@ __device__ __forceinline__ void offsets(const Dims& d, int64_t linear, int64_t* 
   }
 }
 
+// ---- fast unsigned division by a runtime constant (n < 2^31) ------------------------------
+struct FastDiv {
+  uint32_t d, m, s;
+  FastDiv() : d(1), m(0), s(0) {}
+  explicit FastDiv(uint32_t dv) : d(dv) {
+    s = 0;
+    while ((1u << s) < d) ++s;
+    m = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << s) - d)) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+  __device__ __forceinline__ void divmod(uint32_t n, uint32_t& q, uint32_t& r) const {
+    q = div(n);
+    r = n - q * d;
+  }
+};
+
 inline int grid_for(int64_t n, int threads, int per_thread = 1) {
   int64_t blocks = (n + (int64_t)threads * per_thread - 1) / ((int64_t)threads * per_thread);
   int64_t cap = (int64_t)num_sms() * 32;

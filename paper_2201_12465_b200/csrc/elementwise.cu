@@ -16,6 +16,7 @@
 #include <stdint.h>
 #include <type_traits>
 #include <vector>
+#include <cstring>
 #include "common.cuh"
 
 namespace pb {
@@ -225,6 +226,111 @@ __global__ void __launch_bounds__(256) ew_rows_un(RowArgs r) {
   });
 }
 
+
+// ------------------------------------------------------------------ f32 broadcast path
+// f32 operands (or a scalar) with any broadcast strides over <= 4 coalesced axes into a
+// contiguous output.  The reference's hot broadcasts (BatchNorm's per-channel centre /
+// scale, the sum-backward spreads g[n,c,1,1] * ones, bias adds) all land here.
+// ew_bc4: inner extent % 4 == 0 and every tensor operand's inner stride is 1 (16-byte
+//         vector) or 0 (one value per row): 4 float4 per thread, all loads issued first.
+// ew_bc1: anything else: 8 scalars per thread, each decomposed with FastDiv.
+struct BcArgs {
+  const float* a;
+  const float* b;
+  void* out;
+  int nd;               // coalesced rank, 1..4 (axis nd-1 innermost)
+  FastDiv ext[4];       // extents
+  int64_t sa[4], sb[4]; // element strides
+  uint32_t n;           // elements (ew_bc1) or float4s (ew_bc4)
+  int va, vb;           // ew_bc4: inner stride 1 (else 0)
+};
+
+__device__ __forceinline__ void bc_offsets(const BcArgs& p, uint32_t e, int64_t& oa, int64_t& ob) {
+  oa = 0;
+  ob = 0;
+#pragma unroll
+  for (int k = 3; k >= 0; --k) {
+    if (k < p.nd) {
+      uint32_t q, r;
+      if (k > 0) {
+        p.ext[k].divmod(e, q, r);
+      } else {
+        q = 0;
+        r = e;
+      }
+      oa += (int64_t)r * p.sa[k];
+      ob += (int64_t)r * p.sb[k];
+      e = q;
+    }
+  }
+}
+
+template <typename R> struct Out4 { typedef float4 type; };
+template <> struct Out4<bool> { typedef uchar4 type; };
+__device__ __forceinline__ float4 mk4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
+__device__ __forceinline__ uchar4 mk4(bool a, bool b, bool c, bool d) { return make_uchar4(a, b, c, d); }
+
+template <int OP, int AM, int BM>
+__global__ void __launch_bounds__(256) ew_bc4(BcArgs p, float sa, float sb) {
+  typedef typename Bin<OP, float>::res R;
+  typedef typename Out4<R>::type O4;
+  const uint32_t step = gridDim.x * 1024u;
+  for (uint32_t base = blockIdx.x * 1024u + threadIdx.x; base < p.n; base += step) {
+    float4 xa[4], xb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t v = base + u * 256u;
+      xa[u] = make_float4(sa, sa, sa, sa);
+      xb[u] = make_float4(sb, sb, sb, sb);
+      if (v < p.n) {
+        int64_t oa, ob;
+        bc_offsets(p, v * 4u, oa, ob);
+        if (!AM) {
+          if (p.va) xa[u] = __ldg(reinterpret_cast<const float4*>(p.a + oa));
+          else { float t = __ldg(p.a + oa); xa[u] = make_float4(t, t, t, t); }
+        }
+        if (!BM) {
+          if (p.vb) xb[u] = __ldg(reinterpret_cast<const float4*>(p.b + ob));
+          else { float t = __ldg(p.b + ob); xb[u] = make_float4(t, t, t, t); }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t v = base + u * 256u;
+      if (v < p.n)
+        reinterpret_cast<O4*>(p.out)[v] = mk4(Bin<OP, float>::f(xa[u].x, xb[u].x), Bin<OP, float>::f(xa[u].y, xb[u].y),
+                                              Bin<OP, float>::f(xa[u].z, xb[u].z), Bin<OP, float>::f(xa[u].w, xb[u].w));
+    }
+  }
+}
+
+template <int OP, int AM, int BM>
+__global__ void __launch_bounds__(256) ew_bc1(BcArgs p, float sa, float sb) {
+  typedef typename Bin<OP, float>::res R;
+  const uint32_t step = gridDim.x * 2048u;
+  for (uint32_t base = blockIdx.x * 2048u + threadIdx.x; base < p.n; base += step) {
+    float xa[8], xb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t e = base + u * 256u;
+      xa[u] = sa;
+      xb[u] = sb;
+      if (e < p.n) {
+        int64_t oa, ob;
+        bc_offsets(p, e, oa, ob);
+        if (!AM) xa[u] = __ldg(p.a + oa);
+        if (!BM) xb[u] = __ldg(p.b + ob);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t e = base + u * 256u;
+      if (e < p.n) reinterpret_cast<R*>(p.out)[e] = Bin<OP, float>::f(xa[u], xb[u]);
+    }
+  }
+}
+
 // ----------------------------------------------------------------------- host helpers
 static void fill_dims(Dims& d, const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
   d.ndim = out->ndim;
@@ -300,6 +406,69 @@ static int launch_vec_bin(const pb_tensor* a, const pb_tensor* b, int am, int bm
   return PB_OK;
 }
 
+
+// f32 broadcast fast path; returns 1 when launched, 0 when the shape does not qualify
+template <int OP>
+static int try_bcast_f32(const pb_tensor* a, const pb_tensor* b, float sa, float sb, const pb_tensor* out, int* rc) {
+  typedef typename Bin<OP, float>::res R;
+  const int rt = std::is_same<R, bool>::value ? PB_BOOL : PB_F32;
+  if (out->dtype != rt || !is_contiguous(*out) || !aligned16(out->ptr)) return 0;
+  if ((a && a->dtype != PB_F32) || (b && b->dtype != PB_F32)) return 0;
+  int64_t n = numel(*out);
+  if (n <= 0 || n >= ((int64_t)1 << 31)) return 0;
+  Dims d;
+  fill_dims(d, out, a, b);
+  coalesce(d, 3);
+  if (d.ndim > 4) return 0;
+  BcArgs p;
+  p.a = a ? (const float*)(uintptr_t)a->ptr : nullptr;
+  p.b = b ? (const float*)(uintptr_t)b->ptr : nullptr;
+  p.out = (void*)(uintptr_t)out->ptr;
+  p.nd = d.ndim;
+  for (int k = 0; k < 4; ++k) {
+    p.ext[k] = FastDiv(k < d.ndim ? (uint32_t)d.shape[k] : 1u);
+    p.sa[k] = k < d.ndim ? d.st[0][k] : 0;
+    p.sb[k] = k < d.ndim ? d.st[1][k] : 0;
+  }
+  const int in = d.ndim - 1;
+  bool v4 = d.shape[in] % 4 == 0;
+  const pb_tensor* ops[2] = {a, b};
+  int vec[2] = {0, 0};
+  for (int o = 0; o < 2 && v4; ++o) {
+    if (!ops[o]) continue;
+    int64_t is = d.st[o][in];
+    if (is == 1) {
+      vec[o] = 1;
+      if (!aligned16(ops[o]->ptr)) v4 = false;
+      for (int k = 0; k < in; ++k)
+        if (d.st[o][k] % 4) v4 = false;
+    } else if (is != 0) {
+      v4 = false;
+    }
+  }
+  cudaStream_t s = compute_stream();
+  if (v4) {
+    p.n = (uint32_t)(n / 4);
+    p.va = vec[0];
+    p.vb = vec[1];
+    int grid = grid_for(p.n, 1024);
+    if (a && b) ew_bc4<OP, 0, 0><<<grid, 256, 0, s>>>(p, sa, sb);
+    else if (a) ew_bc4<OP, 0, 1><<<grid, 256, 0, s>>>(p, sa, sb);
+    else ew_bc4<OP, 1, 0><<<grid, 256, 0, s>>>(p, sa, sb);
+  } else {
+    p.n = (uint32_t)n;
+    p.va = p.vb = 0;
+    int grid = grid_for(p.n, 2048);
+    if (a && b) ew_bc1<OP, 0, 0><<<grid, 256, 0, s>>>(p, sa, sb);
+    else if (a) ew_bc1<OP, 0, 1><<<grid, 256, 0, s>>>(p, sa, sb);
+    else ew_bc1<OP, 1, 0><<<grid, 256, 0, s>>>(p, sa, sb);
+  }
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  *rc = e == cudaSuccess ? PB_OK : cuda_fail(e, "pb_binary");
+  return 1;
+}
+
 template <int OP, typename CT>
 static int run_binary(const pb_tensor* a, const pb_tensor* b, const pb_scalar* s, const pb_tensor* out) {
   typedef typename Bin<OP, CT>::res R;
@@ -315,22 +484,12 @@ static int run_binary(const pb_tensor* a, const pb_tensor* b, const pb_scalar* s
   if (ct >= 0 && out->dtype == rt && is_contiguous(*out) && aligned16(out->ptr) && (!a || a->dtype == ct) &&
       (!b || b->dtype == ct)) {
     int va = vec_mode(a, out), vb = vec_mode(b, out);
-    if (va >= 0 && vb >= 0 && !(va == 1 && vb == 1)) {
-      // a broadcast-to-all tensor operand becomes a scalar; read it from its single element
-      if (a && va == 1) {
-        RowArgs r = make_rows(out, a, b);
-        ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, 0, 0);
-        PB_LAUNCHED();
-        return PB_OK;
-      }
-      if (b && vb == 1) {
-        RowArgs r = make_rows(out, a, b);
-        ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, 0, 0);
-        PB_LAUNCHED();
-        return PB_OK;
-      }
+    if (va >= 0 && vb >= 0 && !(va == 1 && vb == 1) && !(a && va == 1) && !(b && vb == 1))
       return launch_vec_bin<OP, CT, R>(a, b, va, vb, sa, sb, out, n);
-    }
+  }
+  if (std::is_same<CT, float>::value) {
+    int rc;
+    if (try_bcast_f32<OP>(a, b, (float)sa, (float)sb, out, &rc)) return rc;
   }
   RowArgs r = make_rows(out, a, b);
   ew_rows_bin<OP, CT><<<rows_grid(r), 256, 0, compute_stream()>>>(r, sa, sb, am, bm);
@@ -428,6 +587,50 @@ __global__ void __launch_bounds__(256) pad_kernel(PadArgs p, T value) {
     }
     T v = inside ? load_as<T>(p.src, p.dts, so) : value;
     store_from<T>(p.out, p.dto, oo, v);
+  }
+}
+
+
+// 4-byte same-dtype pad into a contiguous output, n < 2^31: FastDiv index decomposition,
+// 4 elements per thread with the loads issued first (the reference's max-pool backward is
+// chains of these pads over strided views, minml/autograd.py:667-693).
+struct PadFast {
+  const uint32_t* src;
+  uint32_t* out;
+  int nd;
+  FastDiv ext[PB_MAX_RANK];
+  int64_t sstr[PB_MAX_RANK];
+  int32_t lo[PB_MAX_RANK], sext[PB_MAX_RANK];
+  uint32_t n;
+};
+
+__global__ void __launch_bounds__(256) pad_fast(PadFast p, uint32_t value) {
+  const uint32_t step = gridDim.x * 1024u;
+  for (uint32_t base = blockIdx.x * 1024u + threadIdx.x; base < p.n; base += step) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t e = base + u * 256u;
+      v[u] = value;
+      if (e < p.n) {
+        int64_t so = 0;
+        bool inside = true;
+        for (int k = p.nd - 1; k >= 0; --k) {
+          uint32_t q, r;
+          p.ext[k].divmod(e, q, r);
+          int j = (int)r - p.lo[k];
+          inside = inside && j >= 0 && j < p.sext[k];
+          so += (int64_t)j * p.sstr[k];
+          e = q;
+        }
+        if (inside) v[u] = __ldg(p.src + so);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      uint32_t e = base + u * 256u;
+      if (e < p.n) p.out[e] = v[u];
+    }
   }
 }
 
@@ -554,7 +757,62 @@ int pb_unary(int op, const pb_tensor* a, int compute, const pb_tensor* out) {
 
 int pb_copy(const pb_tensor* src, const pb_tensor* dst) { return run_cast(src, dst); }
 
+static bool pad_fast_path(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, const pb_tensor* out,
+                          int* rc) {
+  int64_t n = numel(*out);
+  if (src->dtype != out->dtype || itemsize(out->dtype) != 4 || !is_contiguous(*out) || n >= ((int64_t)1 << 31))
+    return false;
+  PadFast p;
+  p.src = (const uint32_t*)(uintptr_t)src->ptr;
+  p.out = (uint32_t*)(uintptr_t)out->ptr;
+  // merge an axis into its outer neighbour when neither is padded and src is contiguous across them
+  int nd = 0;
+  int64_t oext[PB_MAX_RANK], sstr[PB_MAX_RANK], sext[PB_MAX_RANK], l[PB_MAX_RANK];
+  for (int k = 0; k < out->ndim; ++k) {
+    int64_t e = out->shape[k], st = src->shape[k] == 1 ? 0 : src->strides[k];
+    if (nd > 0 && lo[k] == 0 && e == src->shape[k] && l[nd - 1] == 0 && oext[nd - 1] == sext[nd - 1] &&
+        sstr[nd - 1] == st * e) {
+      oext[nd - 1] *= e;
+      sext[nd - 1] *= e;
+      sstr[nd - 1] = st;
+      continue;
+    }
+    oext[nd] = e;
+    sext[nd] = src->shape[k];
+    sstr[nd] = st;
+    l[nd] = lo[k];
+    ++nd;
+  }
+  for (int k = 0; k < nd; ++k) {
+    if (oext[k] >= ((int64_t)1 << 31) || l[k] >= ((int64_t)1 << 30) || sext[k] >= ((int64_t)1 << 31)) return false;
+    p.ext[k] = FastDiv((uint32_t)oext[k]);
+    p.sstr[k] = sstr[k];
+    p.lo[k] = (int32_t)l[k];
+    p.sext[k] = (int32_t)sext[k];
+  }
+  p.nd = nd;
+  p.n = (uint32_t)n;
+  uint32_t bits;
+  if (out->dtype == PB_F32) {
+    float f = scalar_as<float>(value);
+    memcpy(&bits, &f, 4);
+  } else {
+    int32_t i = scalar_as<int32_t>(value);
+    memcpy(&bits, &i, 4);
+  }
+  pad_fast<<<grid_for(n, 1024), 256, 0, compute_stream()>>>(p, bits);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  *rc = e == cudaSuccess ? PB_OK : cuda_fail(e, "pb_pad");
+  return true;
+}
+
 int pb_pad(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, const pb_tensor* out) {
+  if (numel(*out) == 0) return PB_OK;
+  {
+    int rc;
+    if (pad_fast_path(src, lo, value, out, &rc)) return rc;
+  }
   PadArgs p;
   p.src = (const void*)(uintptr_t)src->ptr;
   p.out = (void*)(uintptr_t)out->ptr;

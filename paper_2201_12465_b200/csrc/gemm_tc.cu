@@ -1,15 +1,843 @@
-// tcgen05 3xTF32 contraction kernels (placeholder: declines every shape until landed).
+// tcgen05 / TMEM 3xTF32 contraction kernels for sm_100a: matmul (rank-2 and batched
+// rank-3) and conv2d fprop / dgrad / wgrad as implicit GEMMs (minml/kernels.py:166-239).
+//
+// Why 3xTF32: the reference contracts f32 operands in f64 and rounds once
+// (kernels.py:168-169, :176-179); one TF32 pass is ~1e-3 off, which breaks the 1e-5
+// parity bar.  Each f32 operand x is split on the fly into
+// hi = rna_tf32(x) and lo = rna_tf32(x - hi) (x - hi is exact in f32, |lo| <= 2^-11 |x|),
+// and D += Alo*Bhi + Ahi*Blo + Ahi*Bhi: per-product error <= ~2^-22, unbiased.
+//
+// Accumulation: the tensor core aligns each MMA's products to its f32 accumulator and
+// truncates, so (a) the tiny lo-products lose bits against a large accumulator and (b) a
+// long K chain (wgrad: K = N*Ho*Wo = 100352 at ResNet-50 b32) drifts with the chain length.
+// Hence the lo-products accumulate in their own TMEM accumulator ("small", ~2^-11 of the
+// "big" hi*hi one), and the MMA accumulates only `ck` k-blocks (64 k by default) into one
+// of two TMEM buffer pairs; dedicated drain warps tcgen05.ld each finished chunk and add
+// big + small into f32 registers with IEEE round-to-nearest while the MMA fills the other
+// pair.
+//
+// One CTA computes a 128 x BN tile of D[i][j] = sum_k A(i,k) B(j,k):
+//   * warps 0..7 (producers): gather A/B elements through an operand "loader" (the
+//     implicit im2col of the conv, or a strided matmul operand), split hi/lo and store
+//     them K-major into 128B-swizzled shared memory (the UMMA canonical SW128 layout), a
+//     STAGES-deep ring guarded by mbarriers (full: producers -> MMA, empty: tcgen05.commit
+//     -> producers);
+//   * warp 8 (MMA): allocates 2*BN TMEM columns, one thread issues 3 x tcgen05.mma.kind::tf32
+//     (M=128, N=BN, K=8) per 8-wide K step, and commits each stage back to the producers
+//     and each chunk to the drain warps;
+//   * warps 9.. (BN/16 drain warps): tcgen05.ld 32x32b rows of each finished chunk, sum in
+//     registers, and finally store through the output functor.  Rows (TMEM lanes) are
+//     always the unit-stride dimension of the output, so a warp's per-column stores are
+//     coalesced.
+// Small-tile / long-K problems (wgrad, matmul-backward) split K over blockIdx.z into a
+// workspace of f32 partials folded in split order (deterministic).
+#include <cuda_runtime.h>
+#include <stdint.h>
 #include "common.cuh"
 
+namespace pb {
+namespace tc {
+
+constexpr int BM = 128;        // D rows per CTA = TMEM lanes = MMA M
+constexpr int BK = 32;         // f32 per 128-byte swizzled row
+constexpr int NPROD = 256;     // producer threads (8 warps)
+constexpr int MMA_WARP = NPROD / 32;
+static int g_ck = 2;           // k-blocks accumulated in TMEM before a register drain
+constexpr int SMEM_BUDGET = 200 * 1024;
+
+// ---- PTX wrappers ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+template <int COLS>
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
+               "n"(COLS));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <int COLS>
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(COLS));
+}
+
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, f32 accumulate
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// 16 consecutive f32 columns of this thread's TMEM lane (complete after tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: D f32, A/B tf32, both K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// byte offset of the 16-byte chunk `chunk` (k/4) of row `row` in a 128B-swizzled tile
+__device__ __forceinline__ uint32_t swz(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ float rna_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ void split1(float x, float& h, float& l) {
+  h = rna_tf32(x);
+  l = rna_tf32(__fsub_rn(x, h));
+}
+__device__ __forceinline__ void split_store(char* hi_tile, char* lo_tile, uint32_t off, float4 v) {
+  float4 h, l;
+  split1(v.x, h.x, l.x);
+  split1(v.y, h.y, l.y);
+  split1(v.z, h.z, l.z);
+  split1(v.w, h.w, l.w);
+  *reinterpret_cast<float4*>(hi_tile + off) = h;
+  *reinterpret_cast<float4*>(lo_tile + off) = l;
+}
+
+__device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
+
+// =========================================================================================
+// Operand loaders.  A loader describes a logical [rows x K] f32 operand.
+//   KMODE = false: lanes of a warp walk consecutive rows for one 4-wide k chunk (rows are
+//                  the unit-stride dimension in memory);
+//   KMODE = true : 8 lanes cover the 32 k of one row, a warp covers 4 rows (k is unit-stride).
+//   Row row(int r): per-row state, computed once per CTA;  float4 get4(Row, k, kend):
+//   elements k..k+3, zero at or beyond kend / outside the operand.
+// =========================================================================================
+
+// strided rank-3 matrix view X[b][r][k] (matmul operands, any strides)
+template <bool KM, bool VEC>
+struct MatLoader {
+  static constexpr bool KMODE = KM;
+  const float* p;
+  int64_t sb, sr, sk;
+  int R;
+  struct Row {
+    const float* p;
+  };
+  __device__ __forceinline__ Row row(int b, int r) const {
+    Row o;
+    o.p = r < R ? p + (int64_t)b * sb + (int64_t)r * sr : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!rw.p) return v;
+    if (VEC && k + 3 < kend) return __ldg(reinterpret_cast<const float4*>(rw.p + k));
+    const float* q = rw.p + (int64_t)k * sk;
+    if (k < kend) v.x = ldg(q);
+    if (k + 1 < kend) v.y = ldg(q + sk);
+    if (k + 2 < kend) v.z = ldg(q + 2 * sk);
+    if (k + 3 < kend) v.w = ldg(q + 3 * sk);
+    return v;
+  }
+};
+
+struct Geo {
+  int N, C, H, W, F, KH, KW, SH, SW, PH, PW, HO, WO;
+};
+
+// fprop A(i = (n,ho,wo), k = (r,s,c)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]     (rows = pixels)
+// C4: C % 4 == 0, so the 4 k of a chunk share (r,s)
+template <bool C4>
+struct FpropX {
+  static constexpr bool KMODE = false;
+  const float* x;
+  Geo g;
+  FastDiv fC, fKW, fP, fWO;
+  int rows;  // N*HO*WO
+  struct Row {
+    const float* p;  // x + n*C*H*W, nullptr when out of range
+    int ih0, iw0;
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = nullptr;
+    o.ih0 = o.iw0 = 0;
+    if (i < rows) {
+      uint32_t n, pix, ho, wo;
+      fP.divmod(i, n, pix);
+      fWO.divmod(pix, ho, wo);
+      o.p = x + (int64_t)n * g.C * g.H * g.W;
+      o.ih0 = (int)ho * g.SH - g.PH;
+      o.iw0 = (int)wo * g.SW - g.PW;
+    }
+    return o;
+  }
+  __device__ __forceinline__ float one(const Row& rw, int k) const {
+    uint32_t rs, c, r, s;
+    fC.divmod(k, rs, c);
+    fKW.divmod(rs, r, s);
+    int ih = rw.ih0 + (int)r, iw = rw.iw0 + (int)s;
+    if ((unsigned)ih >= (unsigned)g.H || (unsigned)iw >= (unsigned)g.W) return 0.f;
+    return ldg(rw.p + ((int64_t)c * g.H + ih) * g.W + iw);
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!rw.p) return v;
+    if (C4 && k + 3 < kend) {
+      uint32_t rs, c, r, s;
+      fC.divmod(k, rs, c);
+      fKW.divmod(rs, r, s);
+      int ih = rw.ih0 + (int)r, iw = rw.iw0 + (int)s;
+      if ((unsigned)ih >= (unsigned)g.H || (unsigned)iw >= (unsigned)g.W) return v;
+      int64_t hw = (int64_t)g.H * g.W;
+      const float* q = rw.p + (int64_t)c * hw + (int64_t)ih * g.W + iw;
+      v.x = ldg(q);
+      v.y = ldg(q + hw);
+      v.z = ldg(q + 2 * hw);
+      v.w = ldg(q + 3 * hw);
+      return v;
+    }
+    if (k < kend) v.x = one(rw, k);
+    if (k + 1 < kend) v.y = one(rw, k + 1);
+    if (k + 2 < kend) v.z = one(rw, k + 2);
+    if (k + 3 < kend) v.w = one(rw, k + 3);
+    return v;
+  }
+};
+
+// dgrad A(i = (n,h,w), k = (r,s,f)) = g[n, f, (h+ph-r)/sh, (w+pw-s)/sw] when on the stride
+// grid and in range, else 0.  Requires F % 4 == 0.                          (rows = pixels)
+struct DgradG {
+  static constexpr bool KMODE = false;
+  const float* gr;
+  Geo g;
+  FastDiv fF, fKW, fHW, fW;
+  int rows;  // N*H*W
+  struct Row {
+    const float* p;  // g + n*F*HO*WO
+    int hp, wp;      // h + ph, w + pw
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = nullptr;
+    o.hp = o.wp = 0;
+    if (i < rows) {
+      uint32_t n, pix, h, w;
+      fHW.divmod(i, n, pix);
+      fW.divmod(pix, h, w);
+      o.p = gr + (int64_t)n * g.F * g.HO * g.WO;
+      o.hp = (int)h + g.PH;
+      o.wp = (int)w + g.PW;
+    }
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!rw.p || k >= kend) return v;
+    uint32_t rs, f, r, s;
+    fF.divmod(k, rs, f);
+    fKW.divmod(rs, r, s);
+    int hh = rw.hp - (int)r, ww = rw.wp - (int)s;
+    if (hh < 0 || ww < 0) return v;
+    int ho = hh / g.SH, wo = ww / g.SW;
+    if (ho * g.SH != hh || wo * g.SW != ww || ho >= g.HO || wo >= g.WO) return v;
+    int64_t P = (int64_t)g.HO * g.WO;
+    const float* q = rw.p + (int64_t)f * P + (int64_t)ho * g.WO + wo;
+    v.x = ldg(q);
+    if (k + 1 < kend) v.y = ldg(q + P);
+    if (k + 2 < kend) v.z = ldg(q + 2 * P);
+    if (k + 3 < kend) v.w = ldg(q + 3 * P);
+    return v;
+  }
+};
+
+// wgrad A(i = (c,r,s), k = (n,ho,wo)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]        (k-mode)
+struct WgradX {
+  static constexpr bool KMODE = true;
+  const float* x;
+  Geo g;
+  FastDiv fP, fWO, fRS, fKW;
+  int rows;  // C*KH*KW
+  struct Row {
+    const float* p;  // x + c*H*W
+    int roff, soff;  // r - ph, s - pw
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = nullptr;
+    o.roff = o.soff = 0;
+    if (i < rows) {
+      uint32_t c, rs, r, s;
+      fRS.divmod(i, c, rs);
+      fKW.divmod(rs, r, s);
+      o.p = x + (int64_t)c * g.H * g.W;
+      o.roff = (int)r - g.PH;
+      o.soff = (int)s - g.PW;
+    }
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!rw.p || k >= kend) return make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t n, pix, ho, wo;
+    fP.divmod(k, n, pix);
+    fWO.divmod(pix, ho, wo);
+    int64_t chw = (int64_t)g.C * g.H * g.W;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (k + t < kend) {
+        int ih = (int)ho * g.SH + rw.roff, iw = (int)wo * g.SW + rw.soff;
+        if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W)
+          e[t] = ldg(rw.p + (int64_t)n * chw + (int64_t)ih * g.W + iw);
+      }
+      if (++wo == (uint32_t)g.WO) {
+        wo = 0;
+        if (++ho == (uint32_t)g.HO) {
+          ho = 0;
+          ++n;
+        }
+      }
+    }
+    return make_float4(e[0], e[1], e[2], e[3]);
+  }
+};
+
+// wgrad B(j = f, k = (n,p)) = g[n, f, p]                                        (k-mode)
+struct WgradG {
+  static constexpr bool KMODE = true;
+  const float* gr;
+  Geo g;
+  FastDiv fP;
+  int rows;  // F
+  bool vec;  // P % 4 == 0: a chunk never straddles images, 16B aligned
+  struct Row {
+    const float* p;  // g + f*P
+  };
+  __device__ __forceinline__ Row row(int, int f) const {
+    Row o;
+    o.p = f < rows ? gr + (int64_t)f * g.HO * g.WO : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!rw.p || k >= kend) return make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t n, pix;
+    fP.divmod(k, n, pix);
+    int64_t fp = (int64_t)g.F * fP.d;
+    if (vec && k + 3 < kend) return __ldg(reinterpret_cast<const float4*>(rw.p + (int64_t)n * fp + pix));
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if (k + t < kend) e[t] = ldg(rw.p + (int64_t)n * fp + pix);
+      if (++pix == fP.d) {
+        pix = 0;
+        ++n;
+      }
+    }
+    return make_float4(e[0], e[1], e[2], e[3]);
+  }
+};
+
+// =========================================================================================
+// Output functors: put(i, j, v) for one D element; rows i are the unit-stride dimension.
+// =========================================================================================
+struct OutMat {  // C[b][j][i], ld = row pitch (elements)
+  float* p;
+  int Mi, Nj;
+  int64_t ld, sb;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int b, int i) const {
+    Row o;
+    o.p = i < Mi ? p + (int64_t)b * sb + i : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < Nj) rw.p[(int64_t)j * ld] = v;
+  }
+};
+
+struct OutConv {  // out[n][j][pix] for i = (n, pix); optional bias[j]
+  float* p;
+  const float* bias;
+  int Mi, Nj;
+  FastDiv fP;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = nullptr;
+    if (i < Mi) {
+      uint32_t n, pix;
+      fP.divmod(i, n, pix);
+      o.p = p + (int64_t)n * Nj * fP.d + pix;
+    }
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < Nj) {
+      if (bias) v = __fadd_rn(v, __ldg(bias + j));
+      rw.p[(int64_t)j * fP.d] = v;
+    }
+  }
+};
+
+struct OutPartial {  // ws[split][j][i] (fold_partials finishes through the real functor)
+  float* p;
+  int Mi, Nj;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int split, int i) const {
+    Row o;
+    o.p = i < Mi ? p + (int64_t)split * Mi * Nj + i : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < Nj) rw.p[(int64_t)j * Mi] = v;
+  }
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (SMEM_BUDGET - 1024 - 256) / STAGE_BYTES > 6 ? 6 : (SMEM_BUDGET - 1024 - 256) / STAGE_BYTES;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;  // + 1024 alignment slack + barriers
+  static constexpr int A_TASKS = BM * 8 / NPROD;                  // 4
+  static constexpr int B_TASKS = BN * 8 / NPROD;
+  static constexpr uint32_t IDESC = idesc_tf32(BM, BN);
+  static constexpr int NDRAIN = BN / 16;                          // drain warps: 64 columns each
+  static constexpr int THREADS = NPROD + 32 + NDRAIN * 32;
+  static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x {big, small}
+};
+
+// rows/chunk of task t for a tile with `rows` rows
+template <bool KMODE, int ROWS>
+__device__ __forceinline__ void task_pos(int t, int& row, int& chunk) {
+  if (KMODE) {
+    row = t >> 3;
+    chunk = t & 7;
+  } else {
+    row = t % ROWS;
+    chunk = t / ROWS;
+  }
+}
+
+// D[i][j] over k in [kbeg, kend) for i in the 128-row tile blockIdx.x, j in tile blockIdx.y,
+// batch/split blockIdx.z
+template <int BN, class LA, class LB, class OUT>
+__global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
+    tc_gemm_kernel(LA la, LB lb, OUT out, int K, int kper, int batched, int CK) {
+  typedef Cfg<BN> C;
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;  // chunk accumulated (MMA -> drain), per TMEM buffer
+  uint64_t* acce = accf + 2;           // chunk drained (drain -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int z = blockIdx.z;
+  const int b = batched ? z : 0;
+  const int kbeg = batched ? 0 : z * kper;
+  const int kend = min(K, kbeg + kper);
+  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
+  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], NPROD);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&accf[s], 1);
+      mbar_init(&acce[s], C::NDRAIN * 32);
+    }
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == MMA_WARP) {
+    // ===== MMA issuer =====
+    if ((tid & 31) == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % C::STAGES, c = kb / CK, buf = c & 1;
+        const bool first = (kb % CK) == 0;
+        if (first && c >= 2) {
+          mbar_wait(&acce[buf], ((c >> 1) - 1) & 1);
+          tc_fence_after();
+        }
+        mbar_wait(&full[s], (kb / C::STAGES) & 1);
+        tc_fence_after();
+        const uint32_t dbig = tmem + (uint32_t)(buf * 2 * BN), dsmall = dbig + BN;
+        uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+        uint64_t ahi = sw128_desc(base), alo = sw128_desc(base + C::A_BYTES);
+        uint64_t bhi = sw128_desc(base + 2 * C::A_BYTES), blo = sw128_desc(base + 2 * C::A_BYTES + C::B_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along the swizzled row
+          const uint32_t acc = !(first && kk == 0);
+          mma_tf32(dsmall, alo + adv, bhi + adv, C::IDESC, acc);
+          mma_tf32(dsmall, ahi + adv, blo + adv, C::IDESC, 1);
+          mma_tf32(dbig, ahi + adv, bhi + adv, C::IDESC, acc);
+        }
+        mma_commit(&empty[s]);
+        if ((kb % CK) == CK - 1 || kb == nkb - 1) mma_commit(&accf[buf]);
+      }
+    }
+    __syncwarp();
+  } else if (warp < MMA_WARP) {
+    // ===== producers =====
+    typename LA::Row ar[C::A_TASKS];
+    typename LB::Row br[C::B_TASKS];
+    int ach[C::A_TASKS], aro[C::A_TASKS], bch[C::B_TASKS], bro[C::B_TASKS];
+#pragma unroll
+    for (int t = 0; t < C::A_TASKS; ++t) {
+      task_pos<LA::KMODE, BM>(tid + t * NPROD, aro[t], ach[t]);
+      ar[t] = la.row(b, i0 + aro[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < C::B_TASKS; ++t) {
+      task_pos<LB::KMODE, BN>(tid + t * NPROD, bro[t], bch[t]);
+      br[t] = lb.row(b, j0 + bro[t]);
+    }
+    for (int kb = 0; kb < nkb; ++kb) {
+      int s = kb % C::STAGES;
+      if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
+      char* st = smem + s * C::STAGE_BYTES;
+      int k0 = kbeg + kb * BK;
+      float4 av[C::A_TASKS], bv[C::B_TASKS];
+#pragma unroll
+      for (int t = 0; t < C::A_TASKS; ++t) av[t] = la.get4(ar[t], k0 + ach[t] * 4, kend);
+#pragma unroll
+      for (int t = 0; t < C::B_TASKS; ++t) bv[t] = lb.get4(br[t], k0 + bch[t] * 4, kend);
+#pragma unroll
+      for (int t = 0; t < C::A_TASKS; ++t) split_store(st, st + C::A_BYTES, swz(aro[t], ach[t]), av[t]);
+#pragma unroll
+      for (int t = 0; t < C::B_TASKS; ++t)
+        split_store(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, swz(bro[t], bch[t]), bv[t]);
+      fence_proxy_async();
+      mbar_arrive(&full[s]);
+    }
+  } else {
+    // ===== drain + epilogue: TMEM lane quadrant is fixed by warp % 4 =====
+    const int q = warp & 3, cg = (warp - MMA_WARP - 1) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cg * 64);
+    float acc[64];
+#pragma unroll
+    for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+    const int nch = (nkb + CK - 1) / CK;
+    for (int c = 0; c < nch; ++c) {
+      const int buf = c & 1;
+      mbar_wait(&accf[buf], (c >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        uint32_t rb[16], rs[16];
+        tmem_ld16(lane_base + (uint32_t)(buf * 2 * BN + p * 16), rb);
+        tmem_ld16(lane_base + (uint32_t)(buf * 2 * BN + BN + p * 16), rs);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          acc[p * 16 + e] = __fadd_rn(acc[p * 16 + e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
+      }
+      tc_fence_before();
+      mbar_arrive(&acce[buf]);
+    }
+    const int i = i0 + q * 32 + (tid & 31);
+    typename OUT::Row orow = out.row(z, i);
+#pragma unroll
+    for (int e = 0; e < 64; ++e) out.put(orow, j0 + cg * 64 + e, acc[e]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// fold split-K partials ws[split][j][i] in split order and store through OUT
+template <class OUT>
+__global__ void fold_partials(const float* ws, int splits, int Mi, int Nj, OUT out) {
+  int64_t MN = (int64_t)Mi * Nj;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < MN;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    float v = ws[idx];
+    for (int s = 1; s < splits; ++s) v = __fadd_rn(v, ws[(int64_t)s * MN + idx]);
+    int j = (int)(idx / Mi), i = (int)(idx - (int64_t)j * Mi);
+    out.put(out.row(0, i), j, v);
+  }
+}
+
+// weight re-layout: dst[a][(r*KW+s)*Bn + bb] = w[f][c][r][s] with (a,bb) = (f,c) (fprop,
+// k = (r,s,c)) or (c,f) (dgrad, k = (r,s,f))
+__global__ void weight_rsk(const float* w, float* dst, int F, int Cc, int RS, int dgrad) {
+  int64_t n = (int64_t)F * Cc * RS;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    int rs = (int)(idx % RS);
+    int64_t t = idx / RS;
+    int c = (int)(t % Cc);
+    int f = (int)(t / Cc);
+    float v = w[idx];
+    if (!dgrad)
+      dst[((int64_t)f * RS + rs) * Cc + c] = v;
+    else
+      dst[((int64_t)c * RS + rs) * F + f] = v;
+  }
+}
+
+// ---- host side --------------------------------------------------------------------------
+template <int BN, class LA, class LB, class OUT>
+static int launch(const LA& la, const LB& lb, const OUT& out, int Mi, int Nj, int K, int zdim, int kper,
+                  int batched) {
+  typedef Cfg<BN> C;
+  static bool attr = false;
+  if (!attr) {
+    PB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<BN, LA, LB, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 C::SMEM));
+    attr = true;
+  }
+  dim3 grid((Mi + BM - 1) / BM, (Nj + BN - 1) / BN, zdim);
+  tc_gemm_kernel<BN, LA, LB, OUT><<<grid, C::THREADS, C::SMEM, compute_stream()>>>(la, lb, out, K, kper, batched, g_ck);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+static int pick_bn(int Nj) { return Nj <= 64 ? 64 : 128; }
+
+// number of K splits so that tiles * splits covers the machine; kper a multiple of BK
+static int pick_splits(int64_t tiles, int K, int* kper) {
+  int splits = 1;
+  int64_t want = num_sms();
+  if (tiles < want && K >= 8 * BK) {
+    splits = (int)((want + tiles - 1) / tiles);
+    int maxs = K / (4 * BK);
+    if (splits > maxs) splits = maxs;
+    if (splits < 1) splits = 1;
+  }
+  int per = (K + splits - 1) / splits;
+  per = (per + BK - 1) / BK * BK;
+  splits = (K + per - 1) / per;
+  *kper = per;
+  return splits;
+}
+
+// run D = A B^T (Mi x Nj over K) into OUT, split-K through the workspace when it helps
+template <int BN, class LA, class LB, class OUT>
+static int run(const LA& la, const LB& lb, const OUT& out, int Mi, int Nj, int K, int batch, float* ws_after) {
+  if (batch > 1) return launch<BN>(la, lb, out, Mi, Nj, K, batch, K, 1);
+  int64_t tiles = (int64_t)((Mi + BM - 1) / BM) * ((Nj + BN - 1) / BN);
+  int kper;
+  int splits = pick_splits(tiles, K, &kper);
+  if (splits == 1) return launch<BN>(la, lb, out, Mi, Nj, K, 1, K, 0);
+  OutPartial part{ws_after, Mi, Nj};
+  int rc = launch<BN>(la, lb, part, Mi, Nj, K, splits, kper, 0);
+  if (rc) return rc;
+  fold_partials<OUT><<<grid_for((int64_t)Mi * Nj, 256), 256, 0, compute_stream()>>>(ws_after, splits, Mi, Nj, out);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+template <class LA, class LB, class OUT>
+static int run_bn(const LA& la, const LB& lb, const OUT& out, int Mi, int Nj, int K, int batch, float* ws) {
+  if (pick_bn(Nj) == 64) return run<64>(la, lb, out, Mi, Nj, K, batch, ws);
+  return run<128>(la, lb, out, Mi, Nj, K, batch, ws);
+}
+
+static size_t split_ws_bytes(int Mi, int Nj) {
+  // worst case splits <= num_sms
+  return (size_t)num_sms() * Mi * Nj * sizeof(float);
+}
+
+static Geo geo(const int64_t* xs, const int64_t* ws, const pb_conv* p) {
+  Geo g;
+  g.N = (int)xs[0];
+  g.C = (int)xs[1];
+  g.H = (int)xs[2];
+  g.W = (int)xs[3];
+  g.F = (int)ws[0];
+  g.KH = (int)ws[2];
+  g.KW = (int)ws[3];
+  g.SH = p->stride_h;
+  g.SW = p->stride_w;
+  g.PH = p->pad_h;
+  g.PW = p->pad_w;
+  g.HO = (g.H + 2 * g.PH - g.KH) / g.SH + 1;
+  g.WO = (g.W + 2 * g.PW - g.KW) / g.SW + 1;
+  return g;
+}
+
+static bool f32_all(const pb_tensor* a, const pb_tensor* b, const pb_tensor* o) {
+  return a->dtype == PB_F32 && b->dtype == PB_F32 && o->dtype == PB_F32;
+}
+static bool fits_i32(int64_t v) { return v < ((int64_t)1 << 31) - 64; }
+
+}  // namespace tc
+}  // namespace pb
+
+using namespace pb;
+using namespace pb::tc;
+
 extern "C" {
-int pb_matmul_tc(const pb_tensor*, const pb_tensor*, const pb_tensor*) { return PB_ERR_UNSUPPORTED; }
-int pb_conv2d_tc(const pb_tensor*, const pb_tensor*, const pb_tensor*, const pb_conv*, const pb_tensor*) {
-  return PB_ERR_UNSUPPORTED;
+
+// experiment hook (not part of the public ABI): k-blocks per TMEM accumulation chunk
+int pb_tc_set_chunk(int ck) {
+  if (ck < 1) return PB_ERR_ARG;
+  g_ck = ck;
+  return PB_OK;
 }
-int pb_conv2d_grad_input_tc(const pb_tensor*, const pb_tensor*, const pb_conv*, const pb_tensor*) {
-  return PB_ERR_UNSUPPORTED;
+
+int pb_matmul_tc(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
+  if (!f32_all(a, b, out)) return PB_ERR_UNSUPPORTED;
+  int r3 = a->ndim == 3;
+  int batch = r3 ? (int)a->shape[0] : 1;
+  int64_t M = a->shape[r3], K = a->shape[r3 + 1], N = b->shape[r3 + 1];
+  if (M * N * batch == 0 || K == 0) return PB_ERR_UNSUPPORTED;  // SIMT handles the trivial cases
+  if (!fits_i32(M * N) || !fits_i32(K) || !fits_i32(M) || !fits_i32(N)) return PB_ERR_UNSUPPORTED;
+  // D[i = n][j = m] = sum_k B[k][n] A[m][k]: rows of D are output columns (unit stride)
+  int64_t bsb = r3 ? b->strides[0] : 0, bsk = b->strides[r3], bsn = b->strides[r3 + 1];
+  int64_t asb = r3 ? a->strides[0] : 0, asm_ = a->strides[r3], ask = a->strides[r3 + 1];
+  const float* pa = (const float*)(uintptr_t)a->ptr;
+  const float* pbp = (const float*)(uintptr_t)b->ptr;
+  OutMat o{(float*)(uintptr_t)out->ptr, (int)N, (int)M, N, M * N};
+  float* ws = nullptr;
+  if (batch == 1) {
+    ws = (float*)workspace(split_ws_bytes((int)N, (int)M));
+    if (!ws) return fail(PB_ERR_OOM, "matmul: no workspace");
+  }
+  // A-operand (rows n): n-stride 1 -> row-mode; else k-mode over B's k-stride
+  // B-operand (rows m): k-stride 1 -> k-mode vectorised when 16B aligned
+  bool avec = ask == 1 && (K % 4 == 0) && (asm_ % 4 == 0) && (asb % 4 == 0) && (a->ptr % 16 == 0);
+  if (bsn == 1) {
+    MatLoader<false, false> la{pbp, bsb, bsn, bsk, (int)N};
+    if (ask == 1) {
+      if (avec) return run_bn(la, MatLoader<true, true>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
+      return run_bn(la, MatLoader<true, false>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
+    }
+    return run_bn(la, MatLoader<false, false>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
+  }
+  MatLoader<true, false> la{pbp, bsb, bsn, bsk, (int)N};
+  if (ask == 1) {
+    if (avec) return run_bn(la, MatLoader<true, true>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
+    return run_bn(la, MatLoader<true, false>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
+  }
+  return run_bn(la, MatLoader<false, false>{pa, asb, asm_, ask, (int)M}, o, (int)N, (int)M, (int)K, batch, ws);
 }
-int pb_conv2d_grad_weight_tc(const pb_tensor*, const pb_tensor*, const pb_conv*, const pb_tensor*) {
-  return PB_ERR_UNSUPPORTED;
+
+int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p,
+                 const pb_tensor* out) {
+  if (!f32_all(x, w, out) || (bias && bias->dtype != PB_F32)) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*x) || !is_contiguous(*w)) return PB_ERR_UNSUPPORTED;
+  Geo g = geo(x->shape, w->shape, p);
+  int64_t rows = (int64_t)g.N * g.HO * g.WO, K = (int64_t)g.C * g.KH * g.KW;
+  if (rows == 0 || g.F == 0 || K == 0) return PB_ERR_UNSUPPORTED;
+  if (!fits_i32(rows * g.F) || !fits_i32((int64_t)g.N * g.C * g.H * g.W)) return PB_ERR_UNSUPPORTED;
+  size_t wbytes = ((size_t)g.F * K * 4 + 255) / 256 * 256;
+  char* ws = (char*)workspace(wbytes + split_ws_bytes((int)rows, g.F));
+  if (!ws) return fail(PB_ERR_OOM, "conv2d: no workspace");
+  float* wt = (float*)ws;
+  weight_rsk<<<grid_for((int64_t)g.F * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wt, g.F,
+                                                                           g.C, g.KH * g.KW, 0);
+  PB_LAUNCHED();
+  OutConv o{(float*)(uintptr_t)out->ptr, bias ? (const float*)(uintptr_t)bias->ptr : nullptr, (int)rows, g.F,
+            FastDiv((uint32_t)(g.HO * g.WO))};
+  FastDiv fC(g.C), fKW(g.KW), fP(g.HO * g.WO), fWO(g.WO);
+  float* part = (float*)(ws + wbytes);
+  bool c4 = g.C % 4 == 0;
+  if (c4) {
+    FpropX<true> la{(const float*)(uintptr_t)x->ptr, g, fC, fKW, fP, fWO, (int)rows};
+    MatLoader<true, true> lb{wt, 0, K, 1, g.F};
+    return run_bn(la, lb, o, (int)rows, g.F, (int)K, 1, part);
+  }
+  FpropX<false> la{(const float*)(uintptr_t)x->ptr, g, fC, fKW, fP, fWO, (int)rows};
+  MatLoader<true, false> lb{wt, 0, K, 1, g.F};
+  return run_bn(la, lb, o, (int)rows, g.F, (int)K, 1, part);
 }
+
+int pb_conv2d_grad_input_tc(const pb_tensor* gr, const pb_tensor* w, const pb_conv* p, const pb_tensor* out) {
+  if (!f32_all(gr, w, out)) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*gr) || !is_contiguous(*w)) return PB_ERR_UNSUPPORTED;
+  Geo g = geo(out->shape, w->shape, p);
+  int64_t rows = (int64_t)g.N * g.H * g.W, K = (int64_t)g.F * g.KH * g.KW;
+  if (rows == 0 || g.C == 0 || K == 0 || g.F % 4 != 0) return PB_ERR_UNSUPPORTED;
+  if (!fits_i32(rows * g.C) || !fits_i32((int64_t)g.N * g.F * g.HO * g.WO)) return PB_ERR_UNSUPPORTED;
+  size_t wbytes = ((size_t)g.C * K * 4 + 255) / 256 * 256;
+  char* ws = (char*)workspace(wbytes + split_ws_bytes((int)rows, g.C));
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input: no workspace");
+  float* wt = (float*)ws;
+  weight_rsk<<<grid_for((int64_t)g.C * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wt, g.F,
+                                                                           g.C, g.KH * g.KW, 1);
+  PB_LAUNCHED();
+  OutConv o{(float*)(uintptr_t)out->ptr, nullptr, (int)rows, g.C, FastDiv((uint32_t)(g.H * g.W))};
+  DgradG la{(const float*)(uintptr_t)gr->ptr, g, FastDiv(g.F), FastDiv(g.KW), FastDiv(g.H * g.W), FastDiv(g.W),
+            (int)rows};
+  MatLoader<true, true> lb{wt, 0, K, 1, g.C};
+  return run_bn(la, lb, o, (int)rows, g.C, (int)K, 1, (float*)(ws + wbytes));
 }
+
+int pb_conv2d_grad_weight_tc(const pb_tensor* x, const pb_tensor* gr, const pb_conv* p, const pb_tensor* out) {
+  if (!f32_all(x, gr, out)) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*x) || !is_contiguous(*gr)) return PB_ERR_UNSUPPORTED;
+  Geo g = geo(x->shape, out->shape, p);
+  int64_t crs = (int64_t)g.C * g.KH * g.KW, K = (int64_t)g.N * g.HO * g.WO;
+  if (crs == 0 || g.F == 0 || K == 0) return PB_ERR_UNSUPPORTED;
+  if (!fits_i32(K) || !fits_i32((int64_t)g.N * g.C * g.H * g.W) || !fits_i32((int64_t)g.N * g.F * g.HO * g.WO))
+    return PB_ERR_UNSUPPORTED;
+  float* ws = (float*)workspace(split_ws_bytes((int)crs, g.F));
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_weight: no workspace");
+  int P = g.HO * g.WO;
+  // D[i = (c,r,s)][j = f] -> dw[f][c][r][s] = out[j * crs + i]
+  OutMat o{(float*)(uintptr_t)out->ptr, (int)crs, g.F, crs, 0};
+  WgradX la{(const float*)(uintptr_t)x->ptr, g, FastDiv(P), FastDiv(g.WO), FastDiv(g.KH * g.KW), FastDiv(g.KW),
+            (int)crs};
+  WgradG lb{(const float*)(uintptr_t)gr->ptr, g, FastDiv(P), g.F, (P % 4) == 0};
+  return run_bn(la, lb, o, (int)crs, g.F, (int)K, 1, ws);
+}
+
+}  // extern "C"

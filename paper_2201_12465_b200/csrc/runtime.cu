@@ -36,13 +36,11 @@ void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 // ---- scratch ---------------------------------------------------------------------------
 static void* g_ws = nullptr;
 static size_t g_ws_bytes = 0;
+static std::vector<void*> g_ws_retired;  // kept alive: CUDA graphs may have recorded them
 void* workspace(size_t bytes) {
   if (bytes <= g_ws_bytes) return g_ws;
   size_t want = bytes < ((size_t)64 << 20) ? ((size_t)64 << 20) : bytes + (bytes >> 2);
-  if (g_ws) {
-    cudaStreamSynchronize(g_streams[0]);  // previous kernels may still read it
-    cudaFree(g_ws);
-  }
+  if (g_ws) g_ws_retired.push_back(g_ws);
   g_ws = nullptr;
   g_ws_bytes = 0;
   if (cudaMalloc(&g_ws, want) != cudaSuccess) return nullptr;

@@ -21,7 +21,7 @@ import sys
 import numpy as np
 
 from .. import dtypes
-from ..errors import DomainError, DTypeError
+from ..errors import DeviceError, DomainError, DTypeError
 from ..memory import CachingManager, MemoryManager, op_tag
 from ..registry import Backend
 from ..shape import normalize_axis
@@ -121,8 +121,30 @@ def compute_dtype(name, da, other, scalar):
 _INT_RANGE = {"u8": (0, 255), "i32": (-2**31, 2**31 - 1), "i64": (-2**63, 2**63 - 1)}
 
 
+class GraphExec:
+    """An instantiated CUDA graph of compute-stream work (see GpuBackend.capture_begin)."""
+
+    __slots__ = ("backend", "handle")
+
+    def __init__(self, backend, handle):
+        self.backend = backend
+        self.handle = handle
+
+    def launch(self):
+        _lib.check(self.backend._lib.pb_graph_launch(self.handle), "graph launch")
+
+    def __del__(self):
+        lib = _lib._lib
+        if lib is not None and self.handle:
+            lib.pb_graph_destroy(self.handle)
+            self.handle = 0
+
+
 class GpuBackend(Backend):
+    _next_pool = 0
+
     def __init__(self, name="gpu", seed=0, device=0):
+        self._capture_pool = 0
         self._lib = _lib.load()
         _lib.check(self._lib.pb_init(device), "pb_init")
         self.device = device
@@ -217,6 +239,66 @@ class GpuBackend(Backend):
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
 
+    # ------------------------------------------------------------- CUDA graphs
+    def capture_begin(self):
+        """Record the compute stream into a CUDA graph from here on.
+
+        Allocations made while recording come from a private allocator pool that is
+        never flushed, so the addresses baked into the graph stay owned by it; eager
+        work between replays allocates from the default pool."""
+        if self._capture_pool:
+            raise DeviceError("a capture is already in progress")
+        self.synchronize()
+        h, _ = self._bind_or_get()
+        GpuBackend._next_pool += 1
+        self._capture_pool = GpuBackend._next_pool
+        self._lib.pb_mm_pool(h, self._capture_pool)
+        rc = self._lib.pb_graph_begin()
+        if rc:
+            self._lib.pb_mm_pool(h, 0)
+            self._capture_pool = 0
+            _lib.check(rc, "graph capture")
+
+    def capture_end(self):
+        """Finish the recording; returns a ``GraphExec`` whose ``launch()`` replays it."""
+        h, _ = self._bind_or_get()
+        ex = ctypes.c_uint64(0)
+        try:
+            _lib.check(self._lib.pb_graph_end(ctypes.byref(ex)), "graph capture")
+        finally:
+            self._lib.pb_mm_pool(h, 0)
+            self._capture_pool = 0
+        return GraphExec(self, ex.value)
+
+    @property
+    def capturing(self):
+        return bool(self._capture_pool)
+
+    def copy_in(self, tensor, host):
+        """Overwrite a contiguous device tensor with a same-shaped host array (stream-ordered)."""
+        a = tensor.adapter
+        host = np.ascontiguousarray(host, dtype=a.dtype.np)
+        if tuple(host.shape) != tuple(a.shape) or not a.contiguous or a.block is None:
+            raise ValueError("copy_in needs a dense device tensor of the same shape")
+        _lib.check(self._lib.pb_h2d(a.ptr, host.ctypes.data, host.nbytes), "copy_in")
+        if a.host is not None:
+            a.host = host.copy()
+
+    def copy_device(self, dst, src):
+        """dst <- src for two dense same-shaped device tensors (stream-ordered, capturable)."""
+        da, sa = dst.adapter, self._contig(src.adapter)
+        if tuple(da.shape) != tuple(sa.shape) or da.dtype is not sa.dtype or not da.contiguous:
+            raise ValueError("copy_device needs dense tensors of one shape and dtype")
+        if da.ptr != sa.ptr and da.block is not None:
+            _lib.check(self._lib.pb_d2d(da.ptr, sa.ptr, dst.shape.size * da.dtype.itemsize), "copy_device")
+
+    def _bind_or_get(self):
+        try:
+            return self._mm
+        except AttributeError:
+            self._mm = self._bind_manager()
+            return self._mm
+
     def launch_count(self):
         """Kernels this library has launched so far (all backends in the process)."""
         return int(self._lib.pb_launch_count())
@@ -258,6 +340,10 @@ class GpuBackend(Backend):
         return out
 
     def _rand(self, call, args):
+        if self._capture_pool:
+            # the counter offset is reserved on the host (minml/_tensor.py:362-368): a replay
+            # would repeat this draw, so random ops stay out of graphs
+            raise DeviceError(f"{call.name} cannot be recorded into a CUDA graph (host-reserved RNG counter)")
         out = self._new(tuple(call.shape), call.dtype, call.name)
         if out.block is not None:
             p = call.params
@@ -280,6 +366,8 @@ class GpuBackend(Backend):
         a = args[0]
         if a.host is not None:
             return a.host.copy()
+        if self._capture_pool:
+            raise DeviceError("to_host (a device->host sync) cannot be recorded into a CUDA graph")
         res = np.empty(a.shape, dtype=a.dtype.np)
         if res.size == 0:
             return res

@@ -1,7 +1,9 @@
 """The measured unit of work: one optimizer step (semantics of minml/training.py:30-51)."""
 
+import numpy as np
+
 from . import _tensor as T
-from . import nn
+from . import nn, registry
 from .autograd import Variable
 
 
@@ -46,3 +48,130 @@ def train_epoch(model, batches, optimizer, comm=None):
         lm.update(value, len(labels))
         am.update(out, labels)
     return lm.result(), am.result()
+
+
+def _modules(m):
+    yield m
+    for _, c in m._children:
+        yield from _modules(c)
+
+
+class CapturedStep:
+    """``train_step`` replayed from one CUDA graph.
+
+    The reference's front end issues ~4.4k primitives per ResNet-50 step from Python; on a
+    B200 that host work, not the GPU, would set the step time.  The first ``warmup`` calls
+    run eagerly (they settle lazily-created state: dense velocities, rebound BN running
+    statistics, grown scratch).  The next call records one whole step -- zero_grad,
+    forward, cross-entropy, backward, [bucketed allreduce], SGD -- into a CUDA graph, and
+    every later call is: copy the batch into the graph's static input buffers, launch the
+    graph, read the loss.  Results are those of ``train_step``: the same kernels run in
+    the same order on the same buffers.
+
+    State the step rebinds instead of updating in place (e.g. BatchNorm running stats,
+    minml/nn.py:299-300) is copied back into its original buffer at the end of the graph,
+    so every replay reads the previous replay's state.  Random primitives (dropout) cannot
+    be recorded: their counter offset is reserved on the host per call.
+    """
+
+    def __init__(self, model, optimizer, ddp=None, warmup=1):
+        self.model, self.opt, self.ddp = model, optimizer, ddp
+        self.backend = registry.get(model_backend(model))
+        self.warmup = int(warmup)
+        self.calls = 0
+        self.graph = None
+        self.x = self.y = None
+        self.loss = self.out = None
+        self.launches = 0
+
+    def _slots(self):
+        slots = []
+        for i, p in enumerate(self.opt.params):
+            slots.append((p, "data", None))
+        vel = getattr(self.opt, "velocity", None)
+        if vel is not None:
+            for i in range(len(vel)):
+                slots.append((vel, i, None))
+        for m in _modules(self.model):
+            for name in m.buffer_names():
+                slots.append((m, name, None))
+        return slots
+
+    @staticmethod
+    def _get(owner, key):
+        return owner[key] if isinstance(key, int) else getattr(owner, key)
+
+    @staticmethod
+    def _set(owner, key, value):
+        if isinstance(key, int):
+            owner[key] = value
+        else:
+            setattr(owner, key, value)
+
+    def _body(self):
+        xv = Variable(self.x)
+        self.opt.zero_grad()
+        out = self.model(xv)
+        loss = nn.cross_entropy(out, self.y)
+        if self.ddp is not None:
+            self.ddp.backward(loss)
+        else:
+            loss.backward()
+        self.opt.step()
+        return loss, out
+
+    def __call__(self, images, labels):
+        be = self.backend
+        labels = np.asarray(labels)
+        if self.graph is not None:  # nn.cross_entropy's range check, done on the host copy
+            classes = self.out.shape[1]
+            if labels.size and (labels.min() < 0 or labels.max() >= classes):
+                bad = labels[(labels < 0) | (labels >= classes)][0]
+                raise IndexError(f"target {int(bad)} out of range for {classes} classes")
+        if self.x is None:
+            self.x = T.tensor(images, backend=be.name)
+            self.y = T.tensor(labels, backend=be.name)
+        else:
+            be.copy_in(self.x, images)
+            be.copy_in(self.y, labels)
+        self.calls += 1
+        if self.graph is None and self.calls <= self.warmup:
+            loss, out = self._body()
+            return loss.scalar(), out
+        if self.graph is None:
+            self._capture()
+        self.graph.launch()
+        return self.loss.scalar(), self.out
+
+    def _capture(self):
+        be = self.backend
+        slots = [(o, k, self._get(o, k)) for o, k, _ in self._slots()]
+        n0 = be.launch_count()
+        be.capture_begin()
+        try:
+            loss, out = self._body()
+        except BaseException:
+            try:
+                be.capture_end()  # discard the partial recording
+            except Exception:  # noqa: BLE001
+                pass
+            be.synchronize()
+            raise
+        try:
+            for owner, key, before in slots:
+                now = self._get(owner, key)
+                if now is before:
+                    continue
+                b = before.data if isinstance(before, Variable) else before
+                n = now.data if isinstance(now, Variable) else now
+                if b is n or b.adapter.ptr == n.adapter.ptr:
+                    continue
+                be.copy_device(b, n)
+                if isinstance(owner, Variable) or key == "data":
+                    owner.data = b
+                else:
+                    self._set(owner, key, before)
+        finally:
+            self.graph = be.capture_end()
+        self.launches = be.launch_count() - n0  # kernels recorded into the graph (per replay)
+        self.loss, self.out = loss, out

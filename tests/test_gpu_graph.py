@@ -1,0 +1,74 @@
+"""Whole-step CUDA graph replay (training.CapturedStep) against the eager
+``train_step`` (minml/training.py:37-51): the same kernels on the same buffers, so losses,
+parameters, momentum buffers and BatchNorm running statistics must be bit-identical."""
+
+import numpy as np
+import pytest
+
+from frontend_util import BUILDERS
+from gpu_util import gpu_backend
+from paper_2201_12465_b200 import errors, models, optim, training
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(name, be, captured, steps, batch, shape, classes, seed=3):
+    be.seed(seed)
+    model = BUILDERS[name](be.name)
+    opt = optim.SGD(model.params(), lr=0.05, momentum=0.9)
+    r = np.random.default_rng(0)
+    data = [(r.standard_normal((batch,) + shape).astype(np.float32), r.integers(0, classes, batch).astype(np.int64))
+            for _ in range(2)]
+    step = training.CapturedStep(model, opt, warmup=1) if captured else None
+    losses = []
+    for k in range(steps):
+        x, y = data[k % 2]
+        if captured:
+            loss, _ = step(x, y)
+        else:
+            loss, _ = training.train_step(model, x, y, opt)
+        losses.append(loss)
+    params = [p.numpy() for p in model.params()]
+    vel = [v.numpy() for v in opt.velocity]
+    bufs = []
+
+    def walk(m):
+        for nme in m.buffer_names():
+            bufs.append(getattr(m, nme).numpy())
+        for _, c in m._children:
+            walk(c)
+    walk(model)
+    return losses, params, vel, bufs, step
+
+
+@pytest.mark.parametrize("name,shape,classes", [("lenet", (1, 28, 28), 10), ("resnet_tiny", (3, 32, 32), 10)])
+def test_captured_step_bit_identical_to_eager(name, shape, classes):
+    be = gpu_backend()
+    eager = _run(name, be, False, 6, 4, shape, classes)
+    graph = _run(name, be, True, 6, 4, shape, classes)
+    step = graph[4]
+    assert step.graph is not None and step.launches > 20
+    assert eager[0] == graph[0], (eager[0], graph[0])
+    for a, b in zip(eager[1] + eager[2] + eager[3], graph[1] + graph[2] + graph[3]):
+        assert np.array_equal(a, b)
+
+
+def test_captured_step_rejects_dropout_and_bad_targets():
+    be = gpu_backend()
+    be.seed(1)
+    model = models.alexnet(classes=10, image=67, channels=(8, 16, 24, 16, 16), hidden=64, backend=be.name)
+    opt = optim.SGD(model.params(), lr=0.01)
+    step = training.CapturedStep(model, opt, warmup=1)
+    x = np.zeros((2, 3, 67, 67), np.float32)
+    y = np.zeros(2, np.int64)
+    step(x, y)  # eager warm-up is fine
+    with pytest.raises(errors.DeviceError):
+        step(x, y)  # recording a dropout mask is refused
+    be.synchronize()
+    lenet = models.mnist_cnn(backend=be.name)
+    st = training.CapturedStep(lenet, optim.SGD(lenet.params(), lr=0.01), warmup=1)
+    xs = np.zeros((2, 1, 28, 28), np.float32)
+    st(xs, np.zeros(2, np.int64))
+    st(xs, np.zeros(2, np.int64))
+    with pytest.raises(IndexError):
+        st(xs, np.array([0, 10], np.int64))

@@ -1,0 +1,135 @@
+"""Parity of the tcgen05 3xTF32 contraction kernels (csrc/gemm_tc.cu) against the f64
+reference contraction (minml/kernels.py:166-239 computes f32 matmul/conv in f64 and
+rounds once), on every code path the dispatcher can take: row-/k-mode operand loaders,
+vectorised and scalar gathers, strided convs, stride-2 dgrad, split-K wgrad and matmul,
+batched matmul, transposed views, ragged tiles.
+
+Tolerance: rel 1e-5 with the reference's metric |a-b|/max(|a|,|b|,1)."""
+
+import numpy as np
+import pytest
+
+from golden_util import rel_err
+from gpu_util import gpu_backend
+from paper_2201_12465_b200 import _tensor as T
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    be = gpu_backend()
+    assert be._lib.pb_gemm_path() == 1
+    return be
+
+
+def _np_conv(x, w, s, p):
+    """f64 direct convolution (cross-correlation), NCHW."""
+    n, c, h, wd = x.shape
+    f, _, kh, kw = w.shape
+    xp = np.pad(x.astype(np.float64), ((0, 0), (0, 0), (p, p), (p, p)))
+    ho, wo = (h + 2 * p - kh) // s + 1, (wd + 2 * p - kw) // s + 1
+    cols = np.empty((n, c, kh, kw, ho, wo))
+    for r in range(kh):
+        for t in range(kw):
+            cols[:, :, r, t] = xp[:, :, r:r + s * ho:s, t:t + s * wo:s]
+    return np.einsum("ncrshw,fcrs->nfhw", cols, w.astype(np.float64)), cols
+
+
+def _np_dgrad(g, w, xs, s, p):
+    n, c, h, wd = xs
+    f, _, kh, kw = w.shape
+    ho, wo = g.shape[2], g.shape[3]
+    dxp = np.zeros((n, c, h + 2 * p + s, wd + 2 * p + s))
+    for r in range(kh):
+        for t in range(kw):
+            dxp[:, :, r:r + s * ho:s, t:t + s * wo:s] += np.einsum("nfhw,fc->nchw", g.astype(np.float64),
+                                                                 w[:, :, r, t].astype(np.float64))
+    return dxp[:, :, p:p + h, p:p + wd]
+
+
+CONVS = [
+    # (x shape, w shape, stride, pad)
+    ((2, 64, 14, 14), (64, 64, 3, 3), 1, 1),      # C4 fast gather, BN=64
+    ((2, 32, 9, 11), (128, 32, 3, 3), 1, 1),      # ragged pixels, BN=128
+    ((3, 3, 23, 23), (16, 3, 7, 7), 2, 3),        # stem-like: C=3 scalar gather, K=147
+    ((2, 1, 28, 28), (32, 1, 5, 5), 1, 0),        # LeNet conv1: C=1
+    ((2, 64, 15, 15), (96, 64, 1, 1), 2, 0),      # 1x1 stride-2 downsample (dgrad stride grid)
+    ((1, 128, 8, 8), (200, 128, 3, 3), 2, 1),     # stride-2 3x3, F not a tile multiple
+    ((4, 256, 7, 7), (64, 256, 1, 1), 1, 0),      # P = 49 (wgrad scalar g gather)
+]
+
+
+@pytest.mark.parametrize("xs,ws,s,p", CONVS, ids=[f"{a}-{b}-s{c}p{d}" for a, b, c, d in CONVS])
+def test_conv_family_tc(gpu, xs, ws, s, p):
+    r = np.random.default_rng(sum(xs) + sum(ws))
+    x = r.standard_normal(xs).astype(np.float32)
+    w = (r.standard_normal(ws) / np.sqrt(ws[1] * ws[2] * ws[3])).astype(np.float32)
+    b = r.standard_normal(ws[0]).astype(np.float32)
+    tx, tw, tb = (T.tensor(a, backend=gpu.name) for a in (x, w, b))
+    want, cols = _np_conv(x, w, s, p)
+    got = T.conv2d(tx, tw, tb, s, p).to_host_buffer()
+    assert rel_err(got, (want + b[None, :, None, None]).astype(np.float32)) <= TOL
+    got_nb = T.conv2d(tx, tw, None, s, p).to_host_buffer()
+    assert rel_err(got_nb, want.astype(np.float32)) <= TOL
+    g = r.standard_normal(got.shape).astype(np.float32)
+    tg = T.tensor(g, backend=gpu.name)
+    gi = T.conv2d_grad_input(tg, tw, xs, s, p).to_host_buffer()
+    assert rel_err(gi, _np_dgrad(g, w, xs, s, p).astype(np.float32)) <= TOL
+    gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()
+    want_w = np.einsum("ncrshw,nfhw->fcrs", cols, g.astype(np.float64))
+    assert rel_err(gw, want_w.astype(np.float32)) <= TOL
+
+
+MATMULS = [(64, 784, 256), (64, 256, 10), (256, 64, 10), (784, 64, 256), (1000, 17, 3), (1, 1, 1),
+           (130, 4100, 70), (2048, 768, 768)]
+
+
+@pytest.mark.parametrize("m,k,n", MATMULS)
+def test_matmul_layouts_tc(gpu, m, k, n):
+    r = np.random.default_rng(m * 7 + k * 3 + n)
+    a = r.standard_normal((m, k)).astype(np.float32)
+    b = (r.standard_normal((k, n)) / np.sqrt(k)).astype(np.float32)
+    want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
+    ta, tb = T.tensor(a, backend=gpu.name), T.tensor(b, backend=gpu.name)
+    assert rel_err((ta @ tb).to_host_buffer(), want) <= TOL
+    # transposed views for both operands (Linear's W^T and matmul backward): no copies
+    at = T.tensor(np.ascontiguousarray(a.T), backend=gpu.name).transpose()
+    bt = T.tensor(np.ascontiguousarray(b.T), backend=gpu.name).transpose()
+    assert rel_err((at @ tb).to_host_buffer(), want) <= TOL
+    assert rel_err((ta @ bt).to_host_buffer(), want) <= TOL
+    assert rel_err((at @ bt).to_host_buffer(), want) <= TOL
+
+
+def test_batched_matmul_tc(gpu):
+    r = np.random.default_rng(9)
+    a = r.standard_normal((6, 128, 64)).astype(np.float32)
+    b = r.standard_normal((6, 64, 100)).astype(np.float32) / 8
+    want = np.einsum("bmk,bkn->bmn", a.astype(np.float64), b.astype(np.float64)).astype(np.float32)
+    ta, tb = T.tensor(a, backend=gpu.name), T.tensor(b, backend=gpu.name)
+    assert rel_err((ta @ tb).to_host_buffer(), want) <= TOL
+    # attention-style transposed operand: b^T stored as [6,100,64]
+    bt = T.tensor(np.ascontiguousarray(np.transpose(b, (0, 2, 1))), backend=gpu.name).transpose((0, 2, 1))
+    assert rel_err((ta @ bt).to_host_buffer(), want) <= TOL
+
+
+def test_tc_matches_simt_path(gpu):
+    """The SIMT kernels (f64 accumulation) are the in-library reference for the tc path."""
+    r = np.random.default_rng(4)
+    x = r.standard_normal((4, 64, 28, 28)).astype(np.float32)
+    w = (r.standard_normal((128, 64, 3, 3)) / 24).astype(np.float32)
+    tx, tw = T.tensor(x, backend=gpu.name), T.tensor(w, backend=gpu.name)
+    lib = gpu._lib
+    outs = []
+    for path in (1, 0):
+        lib.pb_set_gemm_path(path)
+        try:
+            y = T.conv2d(tx, tw, None, 2, 1)
+            g = T.tensor(np.ones(y.shape, np.float32), backend=gpu.name)
+            outs.append([y.to_host_buffer(), T.conv2d_grad_input(g, tw, x.shape, 2, 1).to_host_buffer(),
+                         T.conv2d_grad_weight(tx, g, w.shape, 2, 1).to_host_buffer()])
+        finally:
+            lib.pb_set_gemm_path(1)
+    for a, b in zip(*outs):
+        assert rel_err(a, b) <= TOL
