@@ -116,6 +116,22 @@ int pb_conv2d_grad_input(const pb_tensor* g, const pb_tensor* w, const pb_conv* 
                          const pb_tensor* out);                            /* kernels.py:213-228 */
 int pb_conv2d_grad_weight(const pb_tensor* x, const pb_tensor* g, const pb_conv* p,
                           const pb_tensor* out);                           /* kernels.py:231-239 */
+/* Fused elementwise chain (backend-internal fusion, SURVEY §8f f1 / minml/deferred.py:146-163):
+ * v = head (leaf 0 broadcast to out, or head_scalar); for each step v = op(v, x) or op(x, v)
+ * with x a leaf (broadcast), a scalar, or v itself; unary steps v = op(v).  f32/bool leaves
+ * (bool = 0/1), every step in f32 with the unfused kernels' functors: bit-identical to running
+ * the primitives one at a time.  out: dense f32 or bool. */
+typedef struct pb_chain_step {
+  int32_t op;      /* pb_binop, or 64 + pb_unop */
+  int32_t kind;    /* 0 unary, 1 leaf, 2 scalar, 3 self */
+  int32_t side;    /* 0: op(v, x), 1: op(x, v) */
+  int32_t leaf;
+  int32_t to_bool; /* PB_CAST target: 1 bool, 0 f32 */
+  int32_t pad_;
+  double scalar;
+} pb_chain_step;
+int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                const pb_chain_step* steps, const pb_tensor* out);
 /* In-place multi-tensor SGD (minml/optim.py:64-72 op for op): for each i,
  * g' = g + wd*p (if wd); v = v*mu + g' (if mu, else v := g'); p = p - v*lr.  f32 only. */
 int pb_sgd(int n, const uint64_t* params_in, const uint64_t* params_out, const uint64_t* grads,

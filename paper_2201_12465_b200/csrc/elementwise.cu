@@ -331,6 +331,196 @@ __global__ void __launch_bounds__(256) ew_bc1(BcArgs p, float sa, float sb) {
   }
 }
 
+
+// ------------------------------------------------------------- fused elementwise chains
+// Backend-internal fusion (the rule of minml/deferred.py:146-163 restated for
+// the GPU): the backend defers f32/bool elementwise primitives and runs a whole linear
+// chain  v = head;  v = op_k(v, operand_k) (or op_k(operand_k, v))  in one pass, reading
+// each leaf once with broadcast strides and writing only the chain's result.  Every step
+// applies the same Bin / Un functor the unfused kernels use, in f32 (bools as 0/1), so a
+// fused chain is bit-identical to running its primitives one by one.
+static const int kChainLeaves = 8;
+static const int kChainSteps = 16;
+
+struct ChainStep {
+  int16_t op;    // pb_binop, or 64 + pb_unop (PB_CAST: to the step's bool flag)
+  int8_t kind;   // 0 unary, 1 leaf, 2 scalar, 3 self (v op v)
+  int8_t side;   // binary: 0 -> op(v, x), 1 -> op(x, v)
+  int8_t leaf;
+  int8_t to_bool;  // cast target (unary PB_CAST)
+  float scalar;
+};
+
+struct ChainArgs {
+  const void* leaf[kChainLeaves];
+  int8_t is_bool[kChainLeaves];
+  int8_t vec[kChainLeaves];  // chain4: inner stride 1 (else 0)
+  int nleaves, nsteps, head_kind;  // head_kind 0: leaf 0, 1: scalar
+  float head_scalar;
+  ChainStep step[kChainSteps];
+  void* out;
+  int out_bool;
+  int nd;
+  FastDiv ext[4];
+  int64_t st[kChainLeaves][4];
+  uint32_t n;
+};
+
+__device__ __forceinline__ float chain_bin(int op, float a, float b) {
+  switch (op) {
+    case PB_ADD: return Bin<PB_ADD, float>::f(a, b);
+    case PB_SUB: return Bin<PB_SUB, float>::f(a, b);
+    case PB_MUL: return Bin<PB_MUL, float>::f(a, b);
+    case PB_DIV: return Bin<PB_DIV, float>::f(a, b);
+    case PB_POW: return Bin<PB_POW, float>::f(a, b);
+    case PB_MIN: return Bin<PB_MIN, float>::f(a, b);
+    case PB_MAX: return Bin<PB_MAX, float>::f(a, b);
+    case PB_EQ: return Bin<PB_EQ, float>::f(a, b) ? 1.f : 0.f;
+    case PB_LT: return Bin<PB_LT, float>::f(a, b) ? 1.f : 0.f;
+    case PB_GT: return Bin<PB_GT, float>::f(a, b) ? 1.f : 0.f;
+    case PB_AND: return (a != 0.f && b != 0.f) ? 1.f : 0.f;
+    default: return (a != 0.f || b != 0.f) ? 1.f : 0.f;  // PB_OR
+  }
+}
+__device__ __forceinline__ float chain_un(int op, int to_bool, float v) {
+  switch (op) {
+    case PB_NEG: return Un<PB_NEG, float>::f(v);
+    case PB_ABS: return Un<PB_ABS, float>::f(v);
+    case PB_EXP: return Un<PB_EXP, float>::f(v);
+    case PB_LOG: return Un<PB_LOG, float>::f(v);
+    case PB_SQRT: return Un<PB_SQRT, float>::f(v);
+    case PB_SIN: return Un<PB_SIN, float>::f(v);
+    case PB_COS: return Un<PB_COS, float>::f(v);
+    case PB_TANH: return Un<PB_TANH, float>::f(v);
+    case PB_NOT: return v == 0.f ? 1.f : 0.f;
+    default: return to_bool ? (v != 0.f ? 1.f : 0.f) : v;  // PB_CAST (NaN -> true, like numpy)
+  }
+}
+
+__device__ __forceinline__ void chain_offsets(const ChainArgs& p, uint32_t e, int64_t* off) {
+#pragma unroll
+  for (int l = 0; l < kChainLeaves; ++l) off[l] = 0;
+#pragma unroll
+  for (int k = 3; k >= 0; --k) {
+    if (k < p.nd) {
+      uint32_t q, r;
+      if (k > 0) {
+        p.ext[k].divmod(e, q, r);
+      } else {
+        q = 0;
+        r = e;
+      }
+#pragma unroll
+      for (int l = 0; l < kChainLeaves; ++l)
+        if (l < p.nleaves) off[l] += (int64_t)r * p.st[l][k];
+      e = q;
+    }
+  }
+}
+
+__device__ __forceinline__ float4 chain_load4(const ChainArgs& p, int l, int64_t off) {
+  if (p.is_bool[l]) {
+    const uint8_t* b = (const uint8_t*)p.leaf[l] + off;
+    if (p.vec[l]) {
+      uchar4 u = *reinterpret_cast<const uchar4*>(b);
+      return make_float4(u.x ? 1.f : 0.f, u.y ? 1.f : 0.f, u.z ? 1.f : 0.f, u.w ? 1.f : 0.f);
+    }
+    float t = *b ? 1.f : 0.f;
+    return make_float4(t, t, t, t);
+  }
+  const float* f = (const float*)p.leaf[l] + off;
+  if (p.vec[l]) return __ldg(reinterpret_cast<const float4*>(f));
+  float t = __ldg(f);
+  return make_float4(t, t, t, t);
+}
+
+// 4 output elements per thread-iteration (inner extent % 4 == 0, leaves unit- or zero-stride inside)
+__global__ void __launch_bounds__(256) ew_chain4(ChainArgs p) {
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t v4 = blockIdx.x * blockDim.x + threadIdx.x; v4 < p.n; v4 += step) {
+    int64_t off[kChainLeaves];
+    chain_offsets(p, v4 * 4u, off);
+    float4 x[kChainLeaves];
+#pragma unroll
+    for (int l = 0; l < kChainLeaves; ++l)
+      if (l < p.nleaves) x[l] = chain_load4(p, l, off[l]);
+    float4 v = p.head_kind == 0 ? x[0] : make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
+    for (int s = 0; s < p.nsteps; ++s) {
+      const ChainStep st = p.step[s];
+      if (st.kind == 0) {
+        v.x = chain_un(st.op - 64, st.to_bool, v.x);
+        v.y = chain_un(st.op - 64, st.to_bool, v.y);
+        v.z = chain_un(st.op - 64, st.to_bool, v.z);
+        v.w = chain_un(st.op - 64, st.to_bool, v.w);
+        continue;
+      }
+      float4 o;
+      if (st.kind == 1) {
+        o = x[0];
+#pragma unroll
+        for (int l = 1; l < kChainLeaves; ++l)
+          if (st.leaf == l) o = x[l];
+      } else if (st.kind == 2) {
+        o = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
+      } else {
+        o = v;
+      }
+      if (st.side == 0) {
+        v.x = chain_bin(st.op, v.x, o.x);
+        v.y = chain_bin(st.op, v.y, o.y);
+        v.z = chain_bin(st.op, v.z, o.z);
+        v.w = chain_bin(st.op, v.w, o.w);
+      } else {
+        v.x = chain_bin(st.op, o.x, v.x);
+        v.y = chain_bin(st.op, o.y, v.y);
+        v.z = chain_bin(st.op, o.z, v.z);
+        v.w = chain_bin(st.op, o.w, v.w);
+      }
+    }
+    if (p.out_bool)
+      reinterpret_cast<uchar4*>(p.out)[v4] = make_uchar4(v.x != 0.f, v.y != 0.f, v.z != 0.f, v.w != 0.f);
+    else
+      reinterpret_cast<float4*>(p.out)[v4] = v;
+  }
+}
+
+// one element per thread-iteration, any strides
+__global__ void __launch_bounds__(256) ew_chain1(ChainArgs p) {
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += step) {
+    int64_t off[kChainLeaves];
+    chain_offsets(p, e, off);
+    float x[kChainLeaves];
+#pragma unroll
+    for (int l = 0; l < kChainLeaves; ++l) {
+      if (l < p.nleaves)
+        x[l] = p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[off[l]] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + off[l]);
+    }
+    float v = p.head_kind == 0 ? x[0] : p.head_scalar;
+    for (int s = 0; s < p.nsteps; ++s) {
+      const ChainStep st = p.step[s];
+      if (st.kind == 0) {
+        v = chain_un(st.op - 64, st.to_bool, v);
+        continue;
+      }
+      float o;
+      if (st.kind == 1) {
+        o = x[0];
+#pragma unroll
+        for (int l = 1; l < kChainLeaves; ++l)
+          if (st.leaf == l) o = x[l];
+      } else {
+        o = st.kind == 2 ? st.scalar : v;
+      }
+      v = st.side == 0 ? chain_bin(st.op, v, o) : chain_bin(st.op, o, v);
+    }
+    if (p.out_bool)
+      ((uint8_t*)p.out)[e] = v != 0.f;
+    else
+      ((float*)p.out)[e] = v;
+  }
+}
+
 // ----------------------------------------------------------------------- host helpers
 static void fill_dims(Dims& d, const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
   d.ndim = out->ndim;
@@ -756,6 +946,107 @@ int pb_unary(int op, const pb_tensor* a, int compute, const pb_tensor* out) {
 }
 
 int pb_copy(const pb_tensor* src, const pb_tensor* dst) { return run_cast(src, dst); }
+
+int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                const pb_chain_step* steps, const pb_tensor* out) {
+  int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  if (nleaves < 0 || nleaves > kChainLeaves || nsteps < 0 || nsteps > kChainSteps ||
+      (head_kind == 0 && nleaves == 0))
+    return fail(PB_ERR_ARG, "pb_ew_chain: bad chain shape");
+  if (n >= ((int64_t)1 << 31) || !is_contiguous(*out) || (out->dtype != PB_F32 && out->dtype != PB_BOOL))
+    return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain: output must be a dense f32/bool tensor < 2^31 elements");
+  ChainArgs p;
+  memset(&p, 0, sizeof(p));
+  p.nleaves = nleaves;
+  p.nsteps = nsteps;
+  p.head_kind = head_kind;
+  p.head_scalar = (float)head_scalar;
+  p.out = (void*)(uintptr_t)out->ptr;
+  p.out_bool = out->dtype == PB_BOOL;
+  for (int k = 0; k < nsteps; ++k) {
+    const pb_chain_step& c = steps[k];
+    if (c.kind == 1 && (c.leaf < 0 || c.leaf >= nleaves)) return fail(PB_ERR_ARG, "pb_ew_chain: bad leaf index");
+    p.step[k].op = (int16_t)c.op;
+    p.step[k].kind = (int8_t)c.kind;
+    p.step[k].side = (int8_t)c.side;
+    p.step[k].leaf = (int8_t)c.leaf;
+    p.step[k].to_bool = (int8_t)c.to_bool;
+    p.step[k].scalar = (float)c.scalar;
+  }
+  // right-aligned broadcast strides of every leaf over the output, then coalesce
+  const int nd0 = out->ndim;
+  int64_t shape[PB_MAX_RANK], st[kChainLeaves + 1][PB_MAX_RANK];
+  for (int k = 0; k < nd0; ++k) {
+    shape[k] = out->shape[k];
+    st[kChainLeaves][k] = out->strides[k];
+  }
+  for (int l = 0; l < nleaves; ++l) {
+    const pb_tensor& t = leaves[l];
+    if (t.dtype != PB_F32 && t.dtype != PB_BOOL) return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain: leaf dtype");
+    p.leaf[l] = (const void*)(uintptr_t)t.ptr;
+    p.is_bool[l] = t.dtype == PB_BOOL;
+    for (int k = 0; k < nd0; ++k) st[l][k] = 0;
+    int off = nd0 - t.ndim;
+    if (off < 0) return fail(PB_ERR_ARG, "pb_ew_chain: leaf rank exceeds output rank");
+    for (int k = 0; k < t.ndim; ++k) st[l][off + k] = t.shape[k] == 1 ? 0 : t.strides[k];
+  }
+  // drop extent-1 axes, merge axes contiguous for every operand
+  int nd = 0;
+  int64_t cs[PB_MAX_RANK], cst[kChainLeaves + 1][PB_MAX_RANK];
+  for (int k = 0; k < nd0; ++k) {
+    if (shape[k] == 1) continue;
+    bool merge = nd > 0;
+    for (int l = 0; l <= kChainLeaves && merge; ++l) {
+      if (l < nleaves || l == kChainLeaves)
+        if (cst[l][nd - 1] != st[l][k] * shape[k]) merge = false;
+    }
+    if (merge) {
+      cs[nd - 1] *= shape[k];
+      for (int l = 0; l <= kChainLeaves; ++l) cst[l][nd - 1] = st[l][k];
+    } else {
+      cs[nd] = shape[k];
+      for (int l = 0; l <= kChainLeaves; ++l) cst[l][nd] = st[l][k];
+      ++nd;
+    }
+  }
+  if (nd == 0) {
+    nd = 1;
+    cs[0] = 1;
+    for (int l = 0; l <= kChainLeaves; ++l) cst[l][0] = 0;
+  }
+  if (nd > 4) return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain: more than 4 non-mergeable axes");
+  p.nd = nd;
+  for (int k = 0; k < 4; ++k) {
+    p.ext[k] = FastDiv(k < nd ? (uint32_t)cs[k] : 1u);
+    for (int l = 0; l < kChainLeaves; ++l) p.st[l][k] = (k < nd && l < nleaves) ? cst[l][k] : 0;
+  }
+  bool v4 = cs[nd - 1] % 4 == 0 && ((out->ptr & 15) == 0);
+  for (int l = 0; l < nleaves && v4; ++l) {
+    int64_t is = cst[l][nd - 1];
+    if (is == 1) {
+      p.vec[l] = 1;
+      uint64_t align = p.is_bool[l] ? 4 : 16;
+      if (leaves[l].ptr % align) v4 = false;
+      for (int k = 0; k < nd - 1; ++k)
+        if (cst[l][k] % 4) v4 = false;
+    } else if (is != 0) {
+      v4 = false;
+    }
+  }
+  cudaStream_t s = compute_stream();
+  if (v4) {
+    p.n = (uint32_t)(n / 4);
+    ew_chain4<<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
+  } else {
+    for (int l = 0; l < kChainLeaves; ++l) p.vec[l] = 0;
+    p.n = (uint32_t)n;
+    ew_chain1<<<grid_for(p.n, 256, 4), 256, 0, s>>>(p);
+  }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
 
 static bool pad_fast_path(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, const pb_tensor* out,
                           int* rc) {

@@ -40,8 +40,6 @@ namespace tc {
 
 constexpr int BM = 128;        // D rows per CTA = TMEM lanes = MMA M
 constexpr int BK = 32;         // f32 per 128-byte swizzled row
-constexpr int NPROD = 256;     // producer threads (8 warps)
-constexpr int MMA_WARP = NPROD / 32;
 static int g_ck = 2;           // k-blocks accumulated in TMEM before a register drain
 constexpr int SMEM_BUDGET = 200 * 1024;
 
@@ -119,14 +117,14 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) {
   return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-__device__ __forceinline__ float rna_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
+// Split x into hi = rna_tf32(x) (integer pipe: add half an ulp, clear 13 bits) and
+// lo = rna_tf32(x - hi); x - hi is exact in f32 and |lo| <= 2^-11 |x|.  +-inf keeps
+// hi = x, lo = 0 (inf * w then gives the reference's inf, not NaN).
 __device__ __forceinline__ void split1(float x, float& h, float& l) {
-  h = rna_tf32(x);
-  l = rna_tf32(__fsub_rn(x, h));
+  uint32_t hb = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  h = __uint_as_float(hb);
+  float d = fabsf(x) == __int_as_float(0x7F800000) ? 0.f : __fsub_rn(x, h);
+  l = __uint_as_float((__float_as_uint(d) + 0x1000u) & 0xFFFFE000u);
 }
 __device__ __forceinline__ void split_store(char* hi_tile, char* lo_tile, uint32_t off, float4 v) {
   float4 h, l;
@@ -141,12 +139,17 @@ __device__ __forceinline__ void split_store(char* hi_tile, char* lo_tile, uint32
 __device__ __forceinline__ float ldg(const float* p) { return __ldg(p); }
 
 // =========================================================================================
-// Operand loaders.  A loader describes a logical [rows x K] f32 operand.
-//   KMODE = false: lanes of a warp walk consecutive rows for one 4-wide k chunk (rows are
-//                  the unit-stride dimension in memory);
-//   KMODE = true : 8 lanes cover the 32 k of one row, a warp covers 4 rows (k is unit-stride).
-//   Row row(int r): per-row state, computed once per CTA;  float4 get4(Row, k, kend):
-//   elements k..k+3, zero at or beyond kend / outside the operand.
+// Operand loaders.  A loader describes a logical [rows x K] f32 operand and one of two
+// thread mappings (fixed per thread for the whole kernel):
+//   row mode (KMODE = false): a thread owns ONE row of the 128/BN-row tile and several
+//     4-wide k chunks; lanes of a warp walk consecutive rows (rows are unit-stride in HBM).
+//       Row row(b, r);  KB kb(const Row&, k0, kend);  float4 get4(const KB&, chunk)
+//   k mode (KMODE = true): a thread owns ONE chunk (k0 + 4*(tid&7) .. +3) of several rows;
+//     8 lanes cover a 128-byte row (k is unit-stride in HBM).
+//       Row row(b, r);  KB kb(chunk, k0, kend);      float4 get4(const Row&, const KB&)
+// KB is the per-(thread, k-block) context, so the index arithmetic that depends only on k
+// (im2col decomposition, bounds) is done once per k-block, not once per element.
+// Elements at or beyond kend, or outside the operand, read as 0.
 // =========================================================================================
 
 // strided rank-3 matrix view X[b][r][k] (matmul operands, any strides)
@@ -164,15 +167,47 @@ struct MatLoader {
     o.p = r < R ? p + (int64_t)b * sb + (int64_t)r * sr : nullptr;
     return o;
   }
-  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+  // row mode
+  struct KBR {
+    const float* q;
+    int n;  // valid k in this k-block
+  };
+  __device__ __forceinline__ KBR kb(const Row& rw, int k0, int kend) const {
+    KBR o;
+    o.q = rw.p ? rw.p + (int64_t)k0 * sk : nullptr;
+    o.n = kend - k0;
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const KBR& c, int chunk) const {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!rw.p) return v;
-    if (VEC && k + 3 < kend) return __ldg(reinterpret_cast<const float4*>(rw.p + k));
-    const float* q = rw.p + (int64_t)k * sk;
-    if (k < kend) v.x = ldg(q);
-    if (k + 1 < kend) v.y = ldg(q + sk);
-    if (k + 2 < kend) v.z = ldg(q + 2 * sk);
-    if (k + 3 < kend) v.w = ldg(q + 3 * sk);
+    if (!c.q) return v;
+    const int k = chunk * 4;
+    const float* q = c.q + (int64_t)k * sk;
+    if (k < c.n) v.x = ldg(q);
+    if (k + 1 < c.n) v.y = ldg(q + sk);
+    if (k + 2 < c.n) v.z = ldg(q + 2 * sk);
+    if (k + 3 < c.n) v.w = ldg(q + 3 * sk);
+    return v;
+  }
+  // k mode
+  struct KBK {
+    int k, n;  // first k of the chunk, valid count (<= 4)
+  };
+  __device__ __forceinline__ KBK kb(int chunk, int k0, int kend) const {
+    KBK o;
+    o.k = k0 + chunk * 4;
+    o.n = kend - o.k;
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, const KBK& c) const {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!rw.p || c.n <= 0) return v;
+    if (VEC && c.n >= 4) return __ldg(reinterpret_cast<const float4*>(rw.p + c.k));
+    const float* q = rw.p + (int64_t)c.k * sk;
+    v.x = ldg(q);
+    if (c.n > 1) v.y = ldg(q + sk);
+    if (c.n > 2) v.z = ldg(q + 2 * sk);
+    if (c.n > 3) v.w = ldg(q + 3 * sk);
     return v;
   }
 };
@@ -181,9 +216,9 @@ struct Geo {
   int N, C, H, W, F, KH, KW, SH, SW, PH, PW, HO, WO;
 };
 
-// fprop A(i = (n,ho,wo), k = (r,s,c)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]     (rows = pixels)
-// C4: C % 4 == 0, so the 4 k of a chunk share (r,s)
-template <bool C4>
+// fprop A(i = (n,ho,wo), k = (r,s,c)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]   (row mode)
+// FAST: C % 32 == 0, so a k-block has one (r, s) and 32 consecutive channels
+template <bool FAST>
 struct FpropX {
   static constexpr bool KMODE = false;
   const float* x;
@@ -208,6 +243,27 @@ struct FpropX {
     }
     return o;
   }
+  struct KBR {
+    const float* q;  // FAST: &x[n, c0, ih, iw] or nullptr (padding / out of range)
+    Row rw;          // generic path
+    int k0, kend;
+  };
+  __device__ __forceinline__ KBR kb(const Row& rw, int k0, int kend) const {
+    KBR o;
+    o.rw = rw;
+    o.k0 = k0;
+    o.kend = kend;
+    o.q = nullptr;
+    if (FAST && rw.p) {
+      uint32_t rs, c0, r, s;
+      fC.divmod(k0, rs, c0);
+      fKW.divmod(rs, r, s);
+      int ih = rw.ih0 + (int)r, iw = rw.iw0 + (int)s;
+      if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W)
+        o.q = rw.p + ((int64_t)c0 * g.H + ih) * g.W + iw;
+    }
+    return o;
+  }
   __device__ __forceinline__ float one(const Row& rw, int k) const {
     uint32_t rs, c, r, s;
     fC.divmod(k, rs, c);
@@ -216,38 +272,37 @@ struct FpropX {
     if ((unsigned)ih >= (unsigned)g.H || (unsigned)iw >= (unsigned)g.W) return 0.f;
     return ldg(rw.p + ((int64_t)c * g.H + ih) * g.W + iw);
   }
-  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
+  __device__ __forceinline__ float4 get4(const KBR& c, int chunk) const {
     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!rw.p) return v;
-    if (C4 && k + 3 < kend) {
-      uint32_t rs, c, r, s;
-      fC.divmod(k, rs, c);
-      fKW.divmod(rs, r, s);
-      int ih = rw.ih0 + (int)r, iw = rw.iw0 + (int)s;
-      if ((unsigned)ih >= (unsigned)g.H || (unsigned)iw >= (unsigned)g.W) return v;
-      int64_t hw = (int64_t)g.H * g.W;
-      const float* q = rw.p + (int64_t)c * hw + (int64_t)ih * g.W + iw;
+    if (FAST) {
+      if (!c.q) return v;
+      const int64_t hw = (int64_t)g.H * g.W;
+      const float* q = c.q + (int64_t)(chunk * 4) * hw;
       v.x = ldg(q);
       v.y = ldg(q + hw);
       v.z = ldg(q + 2 * hw);
       v.w = ldg(q + 3 * hw);
       return v;
     }
-    if (k < kend) v.x = one(rw, k);
-    if (k + 1 < kend) v.y = one(rw, k + 1);
-    if (k + 2 < kend) v.z = one(rw, k + 2);
-    if (k + 3 < kend) v.w = one(rw, k + 3);
+    if (!c.rw.p) return v;
+    const int k = c.k0 + chunk * 4;
+    if (k < c.kend) v.x = one(c.rw, k);
+    if (k + 1 < c.kend) v.y = one(c.rw, k + 1);
+    if (k + 2 < c.kend) v.z = one(c.rw, k + 2);
+    if (k + 3 < c.kend) v.w = one(c.rw, k + 3);
     return v;
   }
 };
 
 // dgrad A(i = (n,h,w), k = (r,s,f)) = g[n, f, (h+ph-r)/sh, (w+pw-s)/sw] when on the stride
-// grid and in range, else 0.  Requires F % 4 == 0.                          (rows = pixels)
+// grid and in range, else 0.                                              (row mode)
+// FAST: F % 32 == 0, so a k-block has one (r, s) and 32 consecutive filters
+template <bool FAST>
 struct DgradG {
   static constexpr bool KMODE = false;
   const float* gr;
   Geo g;
-  FastDiv fF, fKW, fHW, fW;
+  FastDiv fF, fKW, fHW, fW, fSH, fSW;
   int rows;  // N*H*W
   struct Row {
     const float* p;  // g + n*F*HO*WO
@@ -267,27 +322,63 @@ struct DgradG {
     }
     return o;
   }
-  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (!rw.p || k >= kend) return v;
+  // &g[n, f, ho, wo] for k = (r,s,f), or nullptr off the stride grid / out of range
+  __device__ __forceinline__ const float* at(const Row& rw, int k, uint32_t* f_out) const {
     uint32_t rs, f, r, s;
     fF.divmod(k, rs, f);
     fKW.divmod(rs, r, s);
+    *f_out = f;
     int hh = rw.hp - (int)r, ww = rw.wp - (int)s;
-    if (hh < 0 || ww < 0) return v;
-    int ho = hh / g.SH, wo = ww / g.SW;
-    if (ho * g.SH != hh || wo * g.SW != ww || ho >= g.HO || wo >= g.WO) return v;
-    int64_t P = (int64_t)g.HO * g.WO;
-    const float* q = rw.p + (int64_t)f * P + (int64_t)ho * g.WO + wo;
-    v.x = ldg(q);
-    if (k + 1 < kend) v.y = ldg(q + P);
-    if (k + 2 < kend) v.z = ldg(q + 2 * P);
-    if (k + 3 < kend) v.w = ldg(q + 3 * P);
-    return v;
+    if (hh < 0 || ww < 0) return nullptr;
+    uint32_t ho, wo, rh, rw_;
+    fSH.divmod(hh, ho, rh);
+    fSW.divmod(ww, wo, rw_);
+    if (rh | rw_ || ho >= (uint32_t)g.HO || wo >= (uint32_t)g.WO) return nullptr;
+    return rw.p + ((int64_t)f * g.HO + ho) * g.WO + wo;
+  }
+  struct KBR {
+    const float* q;  // FAST: &g[n, f0, ho, wo] or nullptr
+    Row rw;
+    int k0, kend;
+  };
+  __device__ __forceinline__ KBR kb(const Row& rw, int k0, int kend) const {
+    KBR o;
+    o.rw = rw;
+    o.k0 = k0;
+    o.kend = kend;
+    o.q = nullptr;
+    if (FAST && rw.p) {
+      uint32_t f;
+      o.q = at(rw, k0, &f);
+    }
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const KBR& c, int chunk) const {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int64_t P = (int64_t)g.HO * g.WO;
+    if (FAST) {
+      if (!c.q) return v;
+      const float* q = c.q + (int64_t)(chunk * 4) * P;
+      v.x = ldg(q);
+      v.y = ldg(q + P);
+      v.z = ldg(q + 2 * P);
+      v.w = ldg(q + 3 * P);
+      return v;
+    }
+    if (!c.rw.p) return v;
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int k = c.k0 + chunk * 4 + t;
+      uint32_t f;
+      const float* q = k < c.kend ? at(c.rw, k, &f) : nullptr;
+      if (q) e[t] = ldg(q);
+    }
+    return make_float4(e[0], e[1], e[2], e[3]);
   }
 };
 
-// wgrad A(i = (c,r,s), k = (n,ho,wo)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]        (k-mode)
+// wgrad A(i = (c,r,s), k = (n,ho,wo)) = x[n, c, ho*sh-ph+r, wo*sw-pw+s]       (k mode)
 struct WgradX {
   static constexpr bool KMODE = true;
   const float* x;
@@ -295,37 +386,40 @@ struct WgradX {
   FastDiv fP, fWO, fRS, fKW;
   int rows;  // C*KH*KW
   struct Row {
-    const float* p;  // x + c*H*W
-    int roff, soff;  // r - ph, s - pw
+    const float* p;  // x + c*H*W + (r-ph)*W + (s-pw)  (may point before the row: only used when in range)
+    int dr, ds;      // r - ph, s - pw; p == nullptr when out of range
   };
   __device__ __forceinline__ Row row(int, int i) const {
     Row o;
     o.p = nullptr;
-    o.roff = o.soff = 0;
+    o.dr = o.ds = 0;
     if (i < rows) {
       uint32_t c, rs, r, s;
       fRS.divmod(i, c, rs);
       fKW.divmod(rs, r, s);
-      o.p = x + (int64_t)c * g.H * g.W;
-      o.roff = (int)r - g.PH;
-      o.soff = (int)s - g.PW;
+      o.dr = (int)r - g.PH;
+      o.ds = (int)s - g.PW;
+      o.p = x + (int64_t)c * g.H * g.W + (int64_t)o.dr * g.W + o.ds;
     }
     return o;
   }
-  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
-    float e[4] = {0.f, 0.f, 0.f, 0.f};
-    if (!rw.p || k >= kend) return make_float4(0.f, 0.f, 0.f, 0.f);
+  struct KBK {
+    int off[4];     // n*C*H*W + (ho*sh)*W + wo*sw, per element
+    int hs[4], ws[4];  // ho*sh, wo*sw; hs = -2^30 marks k >= kend
+  };
+  __device__ __forceinline__ KBK kb(int chunk, int k0, int kend) const {
+    KBK o;
+    const int k = k0 + chunk * 4;
     uint32_t n, pix, ho, wo;
-    fP.divmod(k, n, pix);
+    fP.divmod(k < kend ? k : 0, n, pix);
     fWO.divmod(pix, ho, wo);
-    int64_t chw = (int64_t)g.C * g.H * g.W;
+    const int chw = g.C * g.H * g.W;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      if (k + t < kend) {
-        int ih = (int)ho * g.SH + rw.roff, iw = (int)wo * g.SW + rw.soff;
-        if ((unsigned)ih < (unsigned)g.H && (unsigned)iw < (unsigned)g.W)
-          e[t] = ldg(rw.p + (int64_t)n * chw + (int64_t)ih * g.W + iw);
-      }
+      const bool ok = k + t < kend;
+      o.hs[t] = ok ? (int)ho * g.SH : -(1 << 30);
+      o.ws[t] = (int)wo * g.SW;
+      o.off[t] = ok ? (int)n * chw + o.hs[t] * g.W + o.ws[t] : 0;
       if (++wo == (uint32_t)g.WO) {
         wo = 0;
         if (++ho == (uint32_t)g.HO) {
@@ -334,11 +428,21 @@ struct WgradX {
         }
       }
     }
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, const KBK& c) const {
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+    if (!rw.p) return make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      if ((unsigned)(c.hs[t] + rw.dr) < (unsigned)g.H && (unsigned)(c.ws[t] + rw.ds) < (unsigned)g.W)
+        e[t] = ldg(rw.p + c.off[t]);
+    }
     return make_float4(e[0], e[1], e[2], e[3]);
   }
 };
 
-// wgrad B(j = f, k = (n,p)) = g[n, f, p]                                        (k-mode)
+// wgrad B(j = f, k = (n,p)) = g[n, f, p]                                        (k mode)
 struct WgradG {
   static constexpr bool KMODE = true;
   const float* gr;
@@ -354,21 +458,31 @@ struct WgradG {
     o.p = f < rows ? gr + (int64_t)f * g.HO * g.WO : nullptr;
     return o;
   }
-  __device__ __forceinline__ float4 get4(const Row& rw, int k, int kend) const {
-    float e[4] = {0.f, 0.f, 0.f, 0.f};
-    if (!rw.p || k >= kend) return make_float4(0.f, 0.f, 0.f, 0.f);
+  struct KBK {
+    int off[4];  // n*F*P + pix per element, -1 when k >= kend
+  };
+  __device__ __forceinline__ KBK kb(int chunk, int k0, int kend) const {
+    KBK o;
+    const int k = k0 + chunk * 4;
     uint32_t n, pix;
-    fP.divmod(k, n, pix);
-    int64_t fp = (int64_t)g.F * fP.d;
-    if (vec && k + 3 < kend) return __ldg(reinterpret_cast<const float4*>(rw.p + (int64_t)n * fp + pix));
+    fP.divmod(k < kend ? k : 0, n, pix);
+    const int fp = g.F * (int)fP.d;
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
-      if (k + t < kend) e[t] = ldg(rw.p + (int64_t)n * fp + pix);
+      o.off[t] = k + t < kend ? (int)n * fp + (int)pix : -1;
       if (++pix == fP.d) {
         pix = 0;
         ++n;
       }
     }
+    return o;
+  }
+  __device__ __forceinline__ float4 get4(const Row& rw, const KBK& c) const {
+    if (!rw.p) return make_float4(0.f, 0.f, 0.f, 0.f);
+    if (vec && c.off[3] >= 0) return __ldg(reinterpret_cast<const float4*>(rw.p + c.off[0]));
+    float e[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) e[t] = c.off[t] >= 0 ? ldg(rw.p + c.off[t]) : 0.f;
     return make_float4(e[0], e[1], e[2], e[3]);
   }
 };
@@ -442,10 +556,14 @@ struct Cfg {
   static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (SMEM_BUDGET - 1024 - 256) / STAGE_BYTES > 6 ? 6 : (SMEM_BUDGET - 1024 - 256) / STAGE_BYTES;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + 256;  // + 1024 alignment slack + barriers
-  static constexpr int A_TASKS = BM * 8 / NPROD;                  // 4
+  // 13 warps either way (416 threads, <= 152 registers each): BN=64 has 8 producer and 4
+  // drain warps, BN=128 4 producer and 8 drain warps; every drain thread holds 64 columns
+  static constexpr int NDRAIN = BN / 16;
+  static constexpr int NPROD = (12 - NDRAIN) * 32;
+  static constexpr int MMA_WARP = NPROD / 32;
+  static constexpr int A_TASKS = BM * 8 / NPROD;
   static constexpr int B_TASKS = BN * 8 / NPROD;
   static constexpr uint32_t IDESC = idesc_tf32(BM, BN);
-  static constexpr int NDRAIN = BN / 16;                          // drain warps: 64 columns each
   static constexpr int THREADS = NPROD + 32 + NDRAIN * 32;
   static constexpr int TMEM_COLS = 4 * BN;  // 2 buffers x {big, small}
 };
@@ -466,7 +584,12 @@ __device__ __forceinline__ void task_pos(int t, int& row, int& chunk) {
 // batch/split blockIdx.z
 template <int BN, class LA, class LB, class OUT>
 __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
-    tc_gemm_kernel(LA la, LB lb, OUT out, int K, int kper, int batched, int CK) {
+    tc_gemm_kernel(LA la, LB lb, OUT out, int K, int kper, int batched, int CK, int tiles_i, int tiles_j,
+                   int ntiles) {
+  // Persistent: CTA b walks tiles b, b + gridDim.x, ... of the (z, i-tile, j-tile) space
+  // (j fastest, so concurrently running CTAs share their A rows through L2).  Stage and
+  // TMEM-chunk counters run on across tiles, so the producers and the MMA start the next
+  // tile while the drain warps are still storing the previous one.
   typedef Cfg<BN> C;
   extern __shared__ uint8_t smem_raw[];
   char* smem = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -478,16 +601,11 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int z = blockIdx.z;
-  const int b = batched ? z : 0;
-  const int kbeg = batched ? 0 : z * kper;
-  const int kend = min(K, kbeg + kper);
-  const int i0 = blockIdx.x * BM, j0 = blockIdx.y * BN;
-  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const int per_z = tiles_i * tiles_j;
 
   if (tid == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(&full[s], NPROD);
+      mbar_init(&full[s], C::NPROD);
       mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
@@ -496,107 +614,166 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  if (warp == C::MMA_WARP) tmem_alloc<C::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == MMA_WARP) {
+  if (warp == C::MMA_WARP) {
     // ===== MMA issuer =====
     if ((tid & 31) == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % C::STAGES, c = kb / CK, buf = c & 1;
-        const bool first = (kb % CK) == 0;
-        if (first && c >= 2) {
-          mbar_wait(&acce[buf], ((c >> 1) - 1) & 1);
+      uint32_t it = 0, cc = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int z = t / per_z;
+        const int kbeg = batched ? 0 : z * kper;
+        const int kend = min(K, kbeg + kper);
+        const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+        uint32_t dbig = 0, dsmall = 0;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const bool first = (kb % CK) == 0;
+          if (first) {
+            const uint32_t buf = cc & 1;
+            if (cc >= 2) {
+              mbar_wait(&acce[buf], ((cc >> 1) - 1) & 1);
+              tc_fence_after();
+            }
+            dbig = tmem + buf * 2 * BN;
+            dsmall = dbig + BN;
+          }
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
-        }
-        mbar_wait(&full[s], (kb / C::STAGES) & 1);
-        tc_fence_after();
-        const uint32_t dbig = tmem + (uint32_t)(buf * 2 * BN), dsmall = dbig + BN;
-        uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
-        uint64_t ahi = sw128_desc(base), alo = sw128_desc(base + C::A_BYTES);
-        uint64_t bhi = sw128_desc(base + 2 * C::A_BYTES), blo = sw128_desc(base + 2 * C::A_BYTES + C::B_BYTES);
+          uint32_t base = smem_u32(smem + s * C::STAGE_BYTES);
+          uint64_t ahi = sw128_desc(base), alo = sw128_desc(base + C::A_BYTES);
+          uint64_t bhi = sw128_desc(base + 2 * C::A_BYTES), blo = sw128_desc(base + 2 * C::A_BYTES + C::B_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < BK / 8; ++kk) {
-          uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along the swizzled row
-          const uint32_t acc = !(first && kk == 0);
-          mma_tf32(dsmall, alo + adv, bhi + adv, C::IDESC, acc);
-          mma_tf32(dsmall, ahi + adv, blo + adv, C::IDESC, 1);
-          mma_tf32(dbig, ahi + adv, bhi + adv, C::IDESC, acc);
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            uint64_t adv = (uint64_t)(kk * 32) >> 4;  // 8 tf32 = 32 bytes along the swizzled row
+            const uint32_t acc = !(first && kk == 0);
+            mma_tf32(dsmall, alo + adv, bhi + adv, C::IDESC, acc);
+            mma_tf32(dsmall, ahi + adv, blo + adv, C::IDESC, 1);
+            mma_tf32(dbig, ahi + adv, bhi + adv, C::IDESC, acc);
+          }
+          mma_commit(&empty[s]);
+          if ((kb % CK) == CK - 1 || kb == nkb - 1) {
+            mma_commit(&accf[cc & 1]);
+            ++cc;
+          }
         }
-        mma_commit(&empty[s]);
-        if ((kb % CK) == CK - 1 || kb == nkb - 1) mma_commit(&accf[buf]);
       }
     }
     __syncwarp();
-  } else if (warp < MMA_WARP) {
+  } else if (warp < C::MMA_WARP) {
     // ===== producers =====
-    typename LA::Row ar[C::A_TASKS];
-    typename LB::Row br[C::B_TASKS];
+    // row-mode operands: this thread owns one row (NPROD is a multiple of the tile rows)
+    // and chunks t*NPROD/ROWS + ...; k-mode operands: one chunk (tid & 7) of rows tid/8 + ...
     int ach[C::A_TASKS], aro[C::A_TASKS], bch[C::B_TASKS], bro[C::B_TASKS];
+    uint32_t aoff[C::A_TASKS], boff[C::B_TASKS];
 #pragma unroll
     for (int t = 0; t < C::A_TASKS; ++t) {
-      task_pos<LA::KMODE, BM>(tid + t * NPROD, aro[t], ach[t]);
-      ar[t] = la.row(b, i0 + aro[t]);
+      task_pos<LA::KMODE, BM>(tid + t * C::NPROD, aro[t], ach[t]);
+      aoff[t] = swz(aro[t], ach[t]);
     }
 #pragma unroll
     for (int t = 0; t < C::B_TASKS; ++t) {
-      task_pos<LB::KMODE, BN>(tid + t * NPROD, bro[t], bch[t]);
-      br[t] = lb.row(b, j0 + bro[t]);
+      task_pos<LB::KMODE, BN>(tid + t * C::NPROD, bro[t], bch[t]);
+      boff[t] = swz(bro[t], bch[t]);
     }
-    for (int kb = 0; kb < nkb; ++kb) {
-      int s = kb % C::STAGES;
-      if (kb >= C::STAGES) mbar_wait(&empty[s], ((kb / C::STAGES) - 1) & 1);
-      char* st = smem + s * C::STAGE_BYTES;
-      int k0 = kbeg + kb * BK;
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int z = tile / per_z, rem = tile - z * per_z;
+      const int i0 = (rem / tiles_j) * BM, j0 = (rem % tiles_j) * BN;
+      const int b = batched ? z : 0;
+      const int kbeg = batched ? 0 : z * kper;
+      const int kend = min(K, kbeg + kper);
+      const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+      constexpr int NAR = LA::KMODE ? C::A_TASKS : 1, NBR = LB::KMODE ? C::B_TASKS : 1;
+      typename LA::Row ar[NAR];
+      typename LB::Row br[NBR];
+#pragma unroll
+      for (int t = 0; t < NAR; ++t) ar[t] = la.row(b, i0 + aro[t]);
+#pragma unroll
+      for (int t = 0; t < NBR; ++t) br[t] = lb.row(b, j0 + bro[t]);
       float4 av[C::A_TASKS], bv[C::B_TASKS];
+      auto gather = [&](int k0) {
+        if constexpr (LA::KMODE) {
+          const auto ctx = la.kb(ach[0], k0, kend);
 #pragma unroll
-      for (int t = 0; t < C::A_TASKS; ++t) av[t] = la.get4(ar[t], k0 + ach[t] * 4, kend);
+          for (int t = 0; t < C::A_TASKS; ++t) av[t] = la.get4(ar[t], ctx);
+        } else {
+          const auto ctx = la.kb(ar[0], k0, kend);
 #pragma unroll
-      for (int t = 0; t < C::B_TASKS; ++t) bv[t] = lb.get4(br[t], k0 + bch[t] * 4, kend);
+          for (int t = 0; t < C::A_TASKS; ++t) av[t] = la.get4(ctx, ach[t]);
+        }
+        if constexpr (LB::KMODE) {
+          const auto ctx = lb.kb(bch[0], k0, kend);
 #pragma unroll
-      for (int t = 0; t < C::A_TASKS; ++t) split_store(st, st + C::A_BYTES, swz(aro[t], ach[t]), av[t]);
+          for (int t = 0; t < C::B_TASKS; ++t) bv[t] = lb.get4(br[t], ctx);
+        } else {
+          const auto ctx = lb.kb(br[0], k0, kend);
 #pragma unroll
-      for (int t = 0; t < C::B_TASKS; ++t)
-        split_store(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, swz(bro[t], bch[t]), bv[t]);
-      fence_proxy_async();
-      mbar_arrive(&full[s]);
+          for (int t = 0; t < C::B_TASKS; ++t) bv[t] = lb.get4(ctx, bch[t]);
+        }
+      };
+      // software-pipelined: the gathers for k-block kb+1 are in flight while this thread
+      // waits for a free stage and stores k-block kb
+      if (nkb > 0) gather(kbeg);
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % C::STAGES;
+        if (it >= (uint32_t)C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+        char* st = smem + s * C::STAGE_BYTES;
+#pragma unroll
+        for (int t = 0; t < C::A_TASKS; ++t) split_store(st, st + C::A_BYTES, aoff[t], av[t]);
+#pragma unroll
+        for (int t = 0; t < C::B_TASKS; ++t)
+          split_store(st + 2 * C::A_BYTES, st + 2 * C::A_BYTES + C::B_BYTES, boff[t], bv[t]);
+        fence_proxy_async();
+        mbar_arrive(&full[s]);
+        if (kb + 1 < nkb) gather(kbeg + (kb + 1) * BK);
+      }
     }
   } else {
     // ===== drain + epilogue: TMEM lane quadrant is fixed by warp % 4 =====
-    const int q = warp & 3, cg = (warp - MMA_WARP - 1) >> 2;
+    const int q = warp & 3, cg = (warp - C::MMA_WARP - 1) >> 2;
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cg * 64);
-    float acc[64];
+    uint32_t cc = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int z = tile / per_z, rem = tile - z * per_z;
+      const int i0 = (rem / tiles_j) * BM, j0 = (rem % tiles_j) * BN;
+      const int kbeg = batched ? 0 : z * kper;
+      const int kend = min(K, kbeg + kper);
+      const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+      float acc[64];
 #pragma unroll
-    for (int e = 0; e < 64; ++e) acc[e] = 0.f;
-    const int nch = (nkb + CK - 1) / CK;
-    for (int c = 0; c < nch; ++c) {
-      const int buf = c & 1;
-      mbar_wait(&accf[buf], (c >> 1) & 1);
-      tc_fence_after();
+      for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+      const int nch = (nkb + CK - 1) / CK;
+      for (int c = 0; c < nch; ++c, ++cc) {
+        const uint32_t buf = cc & 1;
+        mbar_wait(&accf[buf], (cc >> 1) & 1);
+        tc_fence_after();
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        uint32_t rb[16], rs[16];
-        tmem_ld16(lane_base + (uint32_t)(buf * 2 * BN + p * 16), rb);
-        tmem_ld16(lane_base + (uint32_t)(buf * 2 * BN + BN + p * 16), rs);
-        tmem_wait_ld();
+        for (int p = 0; p < 4; ++p) {
+          uint32_t rb[16], rs[16];
+          tmem_ld16(lane_base + buf * 2 * BN + (uint32_t)(p * 16), rb);
+          tmem_ld16(lane_base + buf * 2 * BN + BN + (uint32_t)(p * 16), rs);
+          tmem_wait_ld();
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          acc[p * 16 + e] = __fadd_rn(acc[p * 16 + e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
+          for (int e = 0; e < 16; ++e)
+            acc[p * 16 + e] = __fadd_rn(acc[p * 16 + e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
+        }
+        tc_fence_before();
+        mbar_arrive(&acce[buf]);
       }
-      tc_fence_before();
-      mbar_arrive(&acce[buf]);
-    }
-    const int i = i0 + q * 32 + (tid & 31);
-    typename OUT::Row orow = out.row(z, i);
+      const int i = i0 + q * 32 + (tid & 31);
+      typename OUT::Row orow = out.row(z, i);
 #pragma unroll
-    for (int e = 0; e < 64; ++e) out.put(orow, j0 + cg * 64 + e, acc[e]);
+      for (int e = 0; e < 64; ++e) out.put(orow, j0 + cg * 64 + e, acc[e]);
+    }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == MMA_WARP) {
+  if (warp == C::MMA_WARP) {
     tc_fence_after();
     tmem_dealloc<C::TMEM_COLS>(tmem);
   }
@@ -608,10 +785,10 @@ __global__ void fold_partials(const float* ws, int splits, int Mi, int Nj, OUT o
   int64_t MN = (int64_t)Mi * Nj;
   for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < MN;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    float v = ws[idx];
-    for (int s = 1; s < splits; ++s) v = __fadd_rn(v, ws[(int64_t)s * MN + idx]);
+    double v = ws[idx];  // f64: the long-K split sums (wgrad over N*Ho*Wo) add up ~148 partials
+    for (int s = 1; s < splits; ++s) v += (double)ws[(int64_t)s * MN + idx];
     int j = (int)(idx / Mi), i = (int)(idx - (int64_t)j * Mi);
-    out.put(out.row(0, i), j, v);
+    out.put(out.row(0, i), j, (float)v);
   }
 }
 
@@ -643,13 +820,18 @@ static int launch(const LA& la, const LB& lb, const OUT& out, int Mi, int Nj, in
                                  C::SMEM));
     attr = true;
   }
-  dim3 grid((Mi + BM - 1) / BM, (Nj + BN - 1) / BN, zdim);
-  tc_gemm_kernel<BN, LA, LB, OUT><<<grid, C::THREADS, C::SMEM, compute_stream()>>>(la, lb, out, K, kper, batched, g_ck);
+  const int ti = (Mi + BM - 1) / BM, tj = (Nj + BN - 1) / BN;
+  const int64_t ntiles = (int64_t)ti * tj * zdim;
+  if (ntiles >= ((int64_t)1 << 31)) return fail(PB_ERR_UNSUPPORTED, "tc_gemm: too many tiles");
+  const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+  tc_gemm_kernel<BN, LA, LB, OUT><<<grid, C::THREADS, C::SMEM, compute_stream()>>>(la, lb, out, K, kper, batched,
+                                                                                  g_ck, ti, tj, (int)ntiles);
   PB_LAUNCHED();
   return PB_OK;
 }
 
-static int pick_bn(int Nj) { return Nj <= 64 ? 64 : 128; }
+static int g_bn_max = 128;  // widest N tile the dispatcher may pick (experiment hook)
+static int pick_bn(int Nj) { return Nj <= 64 || g_bn_max <= 64 ? 64 : 128; }
 
 // number of K splits so that tiles * splits covers the machine; kper a multiple of BK
 static int pick_splits(int64_t tiles, int K, int* kper) {
@@ -732,6 +914,10 @@ int pb_tc_set_chunk(int ck) {
   g_ck = ck;
   return PB_OK;
 }
+int pb_tc_set_bn_max(int bn) {
+  g_bn_max = bn;
+  return PB_OK;
+}
 
 int pb_matmul_tc(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
   if (!f32_all(a, b, out)) return PB_ERR_UNSUPPORTED;
@@ -789,9 +975,13 @@ int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, 
             FastDiv((uint32_t)(g.HO * g.WO))};
   FastDiv fC(g.C), fKW(g.KW), fP(g.HO * g.WO), fWO(g.WO);
   float* part = (float*)(ws + wbytes);
-  bool c4 = g.C % 4 == 0;
-  if (c4) {
+  if (g.C % 32 == 0) {
     FpropX<true> la{(const float*)(uintptr_t)x->ptr, g, fC, fKW, fP, fWO, (int)rows};
+    MatLoader<true, true> lb{wt, 0, K, 1, g.F};
+    return run_bn(la, lb, o, (int)rows, g.F, (int)K, 1, part);
+  }
+  if (g.C % 4 == 0) {
+    FpropX<false> la{(const float*)(uintptr_t)x->ptr, g, fC, fKW, fP, fWO, (int)rows};
     MatLoader<true, true> lb{wt, 0, K, 1, g.F};
     return run_bn(la, lb, o, (int)rows, g.F, (int)K, 1, part);
   }
@@ -805,7 +995,7 @@ int pb_conv2d_grad_input_tc(const pb_tensor* gr, const pb_tensor* w, const pb_co
   if (!is_contiguous(*gr) || !is_contiguous(*w)) return PB_ERR_UNSUPPORTED;
   Geo g = geo(out->shape, w->shape, p);
   int64_t rows = (int64_t)g.N * g.H * g.W, K = (int64_t)g.F * g.KH * g.KW;
-  if (rows == 0 || g.C == 0 || K == 0 || g.F % 4 != 0) return PB_ERR_UNSUPPORTED;
+  if (rows == 0 || g.C == 0 || K == 0 || g.F % 4 != 0) return PB_ERR_UNSUPPORTED;  // wt rows 16B-aligned
   if (!fits_i32(rows * g.C) || !fits_i32((int64_t)g.N * g.F * g.HO * g.WO)) return PB_ERR_UNSUPPORTED;
   size_t wbytes = ((size_t)g.C * K * 4 + 255) / 256 * 256;
   char* ws = (char*)workspace(wbytes + split_ws_bytes((int)rows, g.C));
@@ -815,9 +1005,14 @@ int pb_conv2d_grad_input_tc(const pb_tensor* gr, const pb_tensor* w, const pb_co
                                                                            g.C, g.KH * g.KW, 1);
   PB_LAUNCHED();
   OutConv o{(float*)(uintptr_t)out->ptr, nullptr, (int)rows, g.C, FastDiv((uint32_t)(g.H * g.W))};
-  DgradG la{(const float*)(uintptr_t)gr->ptr, g, FastDiv(g.F), FastDiv(g.KW), FastDiv(g.H * g.W), FastDiv(g.W),
-            (int)rows};
   MatLoader<true, true> lb{wt, 0, K, 1, g.C};
+  if (g.F % 32 == 0) {
+    DgradG<true> la{(const float*)(uintptr_t)gr->ptr, g, FastDiv(g.F), FastDiv(g.KW), FastDiv(g.H * g.W),
+                    FastDiv(g.W), FastDiv(g.SH), FastDiv(g.SW), (int)rows};
+    return run_bn(la, lb, o, (int)rows, g.C, (int)K, 1, (float*)(ws + wbytes));
+  }
+  DgradG<false> la{(const float*)(uintptr_t)gr->ptr, g, FastDiv(g.F), FastDiv(g.KW), FastDiv(g.H * g.W),
+                   FastDiv(g.W), FastDiv(g.SH), FastDiv(g.SW), (int)rows};
   return run_bn(la, lb, o, (int)rows, g.C, (int)K, 1, (float*)(ws + wbytes));
 }
 

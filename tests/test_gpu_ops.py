@@ -8,7 +8,7 @@ the reference's metric) for transcendental ops, reductions and contractions."""
 import numpy as np
 import pytest
 
-from golden_util import check_against, contraction_tol, op_cases, rel_err
+from golden_util import check_against, contraction_err, op_cases, rel_err
 from gpu_util import gpu_backend
 from paper_2201_12465_b200 import _tensor as T
 from paper_2201_12465_b200 import errors
@@ -122,7 +122,7 @@ def test_matmul_sizes(gpu, m, k, n):
     b = r.standard_normal((k, n)).astype(np.float32) / np.sqrt(k)
     got = (T.tensor(a, backend=gpu.name) @ T.tensor(b, backend=gpu.name)).to_host_buffer()
     want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
-    assert rel_err(got, want) <= contraction_tol(k)
+    assert contraction_err(got, want) <= 1e-5
 
 
 CONV = [((32, 64, 56, 56), (64, 64, 3, 3), 1, 1), ((8, 256, 56, 56), (128, 256, 1, 1), 2, 0),
@@ -142,6 +142,5 @@ def test_conv_sizes(gpu, xs, ws, s, p):
     tg = T.tensor(g, backend=gpu.name)
     gi = T.conv2d_grad_input(tg, tw, xs, s, p).to_host_buffer()
     assert rel_err(gi, _oracle("conv2d_grad_input", dict(params, x_shape=xs), [g, w])) <= 1e-5
-    gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()
-    k = g.shape[0] * g.shape[2] * g.shape[3]  # wgrad reduces over N*Ho*Wo
-    assert rel_err(gw, _oracle("conv2d_grad_weight", dict(params, w_shape=ws), [x, g])) <= contraction_tol(k)
+    gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()  # reduces over N*Ho*Wo (up to 100352)
+    assert contraction_err(gw, _oracle("conv2d_grad_weight", dict(params, w_shape=ws), [x, g])) <= 1e-5

@@ -68,13 +68,16 @@ def main():
         flops = 2 * y.shape.size * ws_[1] * ws_[2] * ws_[3]
         dev.append((xs_, ws_, s_, p_, xx, ww, gg, flops))
 
-    for ck in (1, 2, 4, 8):
+    setbn = lib.pb_tc_set_bn_max
+    setbn.argtypes = [ctypes.c_int]
+    for ck, bn in ((2, 128), (2, 64), (1, 64), (4, 64)):
         setck(ck)
+        setbn(bn)
         e_w = rel_err(T.conv2d_grad_weight(tx, tg, ws, 1, 1).to_host_buffer(), want_w)
         e_f = rel_err(T.conv2d(tx, tw, None, 1, 1).to_host_buffer(), want.astype(np.float32))
         e_l = rel_err(T.conv2d_grad_weight(txl, tgl, (64, 64, 1, 1), 1, 0).to_host_buffer().reshape(64, 64), want_l)
         e_m = rel_err((ta @ tb).to_host_buffer(), want_m)
-        print(f"ck={ck}: wgrad K=392 {e_w:.2e}  fprop K=576 {e_f:.2e}  wgrad K=100352 {e_l:.2e}  "
+        print(f"ck={ck} bn<={bn}: wgrad K=392 {e_w:.2e}  fprop K=576 {e_f:.2e}  wgrad K=100352 {e_l:.2e}  "
               f"matmul K=3072 {e_m:.2e}", flush=True)
         for xs_, ws_, s_, p_, xx, ww, gg, flops in dev:
             res = []
@@ -89,6 +92,7 @@ def main():
                 res.append(f"{name} {ms:.3f} ms {flops / ms / 1e9:.0f} TF/s")
             print(f"   {xs_} * {ws_} s{s_}: " + "; ".join(res), flush=True)
     setck(2)
+    setbn(128)
 
 
 if __name__ == "__main__":
