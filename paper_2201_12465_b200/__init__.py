@@ -23,7 +23,7 @@ if os.environ.get("PB_NO_AUTOREGISTER") != "1":
             registry.register(GpuBackend("gpu", device=int(os.environ.get("LOCAL_RANK", "0")) % _ndev))
         else:
             registry._load_error = "no CUDA device visible"
-    except (OSError, ImportError) as exc:  # libpaper_b200.so missing or unloadable
+    except (OSError, ImportError, AttributeError) as exc:  # libpaper_b200.so missing, unloadable or stale
         registry._load_error = f"libpaper_b200.so not loadable: {exc}"
 
 from . import distributed, nn, ops, optim, training  # noqa: E402

@@ -50,10 +50,12 @@ def build(verbose=False):
     objs = [_obj(s) for s in SOURCES]
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(o) for o in objs):
         return OUT
-    cmd = [NVCC] + ARCH + ["-shared", "-o", OUT] + objs + ["-lnccl", "-lcudart"]
+    tmp = OUT + f".tmp{os.getpid()}"
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lnccl", "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
+    os.replace(tmp, OUT)  # new inode: a process that mapped the old library keeps it intact
     return OUT
 
 

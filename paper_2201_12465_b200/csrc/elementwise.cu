@@ -366,40 +366,10 @@ struct ChainArgs {
   uint32_t n;
 };
 
-__device__ __forceinline__ float chain_bin(int op, float a, float b) {
-  switch (op) {
-    case PB_ADD: return Bin<PB_ADD, float>::f(a, b);
-    case PB_SUB: return Bin<PB_SUB, float>::f(a, b);
-    case PB_MUL: return Bin<PB_MUL, float>::f(a, b);
-    case PB_DIV: return Bin<PB_DIV, float>::f(a, b);
-    case PB_POW: return Bin<PB_POW, float>::f(a, b);
-    case PB_MIN: return Bin<PB_MIN, float>::f(a, b);
-    case PB_MAX: return Bin<PB_MAX, float>::f(a, b);
-    case PB_EQ: return Bin<PB_EQ, float>::f(a, b) ? 1.f : 0.f;
-    case PB_LT: return Bin<PB_LT, float>::f(a, b) ? 1.f : 0.f;
-    case PB_GT: return Bin<PB_GT, float>::f(a, b) ? 1.f : 0.f;
-    case PB_AND: return (a != 0.f && b != 0.f) ? 1.f : 0.f;
-    default: return (a != 0.f || b != 0.f) ? 1.f : 0.f;  // PB_OR
-  }
-}
-__device__ __forceinline__ float chain_un(int op, int to_bool, float v) {
-  switch (op) {
-    case PB_NEG: return Un<PB_NEG, float>::f(v);
-    case PB_ABS: return Un<PB_ABS, float>::f(v);
-    case PB_EXP: return Un<PB_EXP, float>::f(v);
-    case PB_LOG: return Un<PB_LOG, float>::f(v);
-    case PB_SQRT: return Un<PB_SQRT, float>::f(v);
-    case PB_SIN: return Un<PB_SIN, float>::f(v);
-    case PB_COS: return Un<PB_COS, float>::f(v);
-    case PB_TANH: return Un<PB_TANH, float>::f(v);
-    case PB_NOT: return v == 0.f ? 1.f : 0.f;
-    default: return to_bool ? (v != 0.f ? 1.f : 0.f) : v;  // PB_CAST (NaN -> true, like numpy)
-  }
-}
-
+template <int NL>
 __device__ __forceinline__ void chain_offsets(const ChainArgs& p, uint32_t e, int64_t* off) {
 #pragma unroll
-  for (int l = 0; l < kChainLeaves; ++l) off[l] = 0;
+  for (int l = 0; l < NL; ++l) off[l] = 0;
 #pragma unroll
   for (int k = 3; k >= 0; --k) {
     if (k < p.nd) {
@@ -411,8 +381,7 @@ __device__ __forceinline__ void chain_offsets(const ChainArgs& p, uint32_t e, in
         r = e;
       }
 #pragma unroll
-      for (int l = 0; l < kChainLeaves; ++l)
-        if (l < p.nleaves) off[l] += (int64_t)r * p.st[l][k];
+      for (int l = 0; l < NL; ++l) off[l] += (int64_t)r * p.st[l][k];
       e = q;
     }
   }
@@ -434,48 +403,108 @@ __device__ __forceinline__ float4 chain_load4(const ChainArgs& p, int l, int64_t
   return make_float4(t, t, t, t);
 }
 
-// 4 output elements per thread-iteration (inner extent % 4 == 0, leaves unit- or zero-stride inside)
+#define PB_LANES4(...)        \
+  {                           \
+    float a_ = v.x, b_ = o.x; \
+    v.x = __VA_ARGS__;        \
+    a_ = v.y;                 \
+    b_ = o.y;                 \
+    v.y = __VA_ARGS__;        \
+    a_ = v.z;                 \
+    b_ = o.z;                 \
+    v.z = __VA_ARGS__;        \
+    a_ = v.w;                 \
+    b_ = o.w;                 \
+    v.w = __VA_ARGS__;        \
+    (void)b_;                 \
+  }
+
+// one step on 4 lanes; the (warp-uniform) switch is taken once per step, not per lane
+__device__ __forceinline__ float4 chain_step4(const ChainStep& st, float4 v, float4 o) {
+  if (st.kind == 0) {
+    const int op = st.op - 64;
+    switch (op) {
+      case PB_NEG: PB_LANES4(Un<PB_NEG, float>::f(a_)) break;
+      case PB_ABS: PB_LANES4(Un<PB_ABS, float>::f(a_)) break;
+      case PB_EXP: PB_LANES4(Un<PB_EXP, float>::f(a_)) break;
+      case PB_LOG: PB_LANES4(Un<PB_LOG, float>::f(a_)) break;
+      case PB_SQRT: PB_LANES4(Un<PB_SQRT, float>::f(a_)) break;
+      case PB_SIN: PB_LANES4(Un<PB_SIN, float>::f(a_)) break;
+      case PB_COS: PB_LANES4(Un<PB_COS, float>::f(a_)) break;
+      case PB_TANH: PB_LANES4(Un<PB_TANH, float>::f(a_)) break;
+      case PB_NOT: PB_LANES4(a_ == 0.f ? 1.f : 0.f) break;
+      default:
+        if (st.to_bool) PB_LANES4(a_ != 0.f ? 1.f : 0.f)
+        break;
+    }
+    (void)o;
+    return v;
+  }
+  if (st.side) {
+    float4 t = v;
+    v = o;
+    o = t;
+  }
+  switch (st.op) {
+    case PB_ADD: PB_LANES4(Bin<PB_ADD, float>::f(a_, b_)) break;
+    case PB_SUB: PB_LANES4(Bin<PB_SUB, float>::f(a_, b_)) break;
+    case PB_MUL: PB_LANES4(Bin<PB_MUL, float>::f(a_, b_)) break;
+    case PB_DIV: PB_LANES4(Bin<PB_DIV, float>::f(a_, b_)) break;
+    case PB_POW: PB_LANES4(Bin<PB_POW, float>::f(a_, b_)) break;
+    case PB_MIN: PB_LANES4(Bin<PB_MIN, float>::f(a_, b_)) break;
+    case PB_MAX: PB_LANES4(Bin<PB_MAX, float>::f(a_, b_)) break;
+    case PB_EQ: PB_LANES4(a_ == b_ ? 1.f : 0.f) break;
+    case PB_LT: PB_LANES4(a_ < b_ ? 1.f : 0.f) break;
+    case PB_GT: PB_LANES4(a_ > b_ ? 1.f : 0.f) break;
+    case PB_AND: PB_LANES4((a_ != 0.f && b_ != 0.f) ? 1.f : 0.f) break;
+    default: PB_LANES4((a_ != 0.f || b_ != 0.f) ? 1.f : 0.f) break;
+  }
+  return v;
+}
+#undef PB_LANES4
+
+// 4 output elements per thread-iteration (inner extent % 4 == 0, leaves unit- or zero-stride
+// inside); NL = number of leaves, so offsets and leaf values stay in registers
+// leaf values live in eight named registers: selecting one per step with a compare chain
+// (an array here is turned into a local-memory table indexed by st.leaf)
+template <int NL, typename V>
+__device__ __forceinline__ V pick(int l, const V& x0, const V& x1, const V& x2, const V& x3, const V& x4,
+                                  const V& x5, const V& x6, const V& x7) {
+  V o = x0;
+  if (NL > 1 && l == 1) o = x1;
+  if (NL > 2 && l == 2) o = x2;
+  if (NL > 3 && l == 3) o = x3;
+  if (NL > 4 && l == 4) o = x4;
+  if (NL > 5 && l == 5) o = x5;
+  if (NL > 6 && l == 6) o = x6;
+  if (NL > 7 && l == 7) o = x7;
+  return o;
+}
+
+// 4 output elements per thread-iteration (inner extent % 4 == 0, leaves unit- or zero-stride
+// inside); NL = number of leaves, so offsets and leaf values stay in registers
+template <int NL>
 __global__ void __launch_bounds__(256) ew_chain4(ChainArgs p) {
   const uint32_t step = gridDim.x * blockDim.x;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
   for (uint32_t v4 = blockIdx.x * blockDim.x + threadIdx.x; v4 < p.n; v4 += step) {
-    int64_t off[kChainLeaves];
-    chain_offsets(p, v4 * 4u, off);
-    float4 x[kChainLeaves];
-#pragma unroll
-    for (int l = 0; l < kChainLeaves; ++l)
-      if (l < p.nleaves) x[l] = chain_load4(p, l, off[l]);
-    float4 v = p.head_kind == 0 ? x[0] : make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
+    int64_t off[NL];
+    chain_offsets<NL>(p, v4 * 4u, off);
+    float4 x0 = chain_load4(p, 0, off[0]);
+    float4 x1 = NL > 1 ? chain_load4(p, 1, off[NL > 1 ? 1 : 0]) : z;
+    float4 x2 = NL > 2 ? chain_load4(p, 2, off[NL > 2 ? 2 : 0]) : z;
+    float4 x3 = NL > 3 ? chain_load4(p, 3, off[NL > 3 ? 3 : 0]) : z;
+    float4 x4 = NL > 4 ? chain_load4(p, 4, off[NL > 4 ? 4 : 0]) : z;
+    float4 x5 = NL > 5 ? chain_load4(p, 5, off[NL > 5 ? 5 : 0]) : z;
+    float4 x6 = NL > 6 ? chain_load4(p, 6, off[NL > 6 ? 6 : 0]) : z;
+    float4 x7 = NL > 7 ? chain_load4(p, 7, off[NL > 7 ? 7 : 0]) : z;
+    float4 v = p.head_kind == 0 ? x0 : make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
     for (int s = 0; s < p.nsteps; ++s) {
       const ChainStep st = p.step[s];
-      if (st.kind == 0) {
-        v.x = chain_un(st.op - 64, st.to_bool, v.x);
-        v.y = chain_un(st.op - 64, st.to_bool, v.y);
-        v.z = chain_un(st.op - 64, st.to_bool, v.z);
-        v.w = chain_un(st.op - 64, st.to_bool, v.w);
-        continue;
-      }
-      float4 o;
-      if (st.kind == 1) {
-        o = x[0];
-#pragma unroll
-        for (int l = 1; l < kChainLeaves; ++l)
-          if (st.leaf == l) o = x[l];
-      } else if (st.kind == 2) {
-        o = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
-      } else {
-        o = v;
-      }
-      if (st.side == 0) {
-        v.x = chain_bin(st.op, v.x, o.x);
-        v.y = chain_bin(st.op, v.y, o.y);
-        v.z = chain_bin(st.op, v.z, o.z);
-        v.w = chain_bin(st.op, v.w, o.w);
-      } else {
-        v.x = chain_bin(st.op, o.x, v.x);
-        v.y = chain_bin(st.op, o.y, v.y);
-        v.z = chain_bin(st.op, o.z, v.z);
-        v.w = chain_bin(st.op, o.w, v.w);
-      }
+      float4 o = v;
+      if (st.kind == 1) o = pick<NL>(st.leaf, x0, x1, x2, x3, x4, x5, x6, x7);
+      else if (st.kind == 2) o = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
+      v = chain_step4(st, v, o);
     }
     if (p.out_bool)
       reinterpret_cast<uchar4*>(p.out)[v4] = make_uchar4(v.x != 0.f, v.y != 0.f, v.z != 0.f, v.w != 0.f);
@@ -484,41 +513,45 @@ __global__ void __launch_bounds__(256) ew_chain4(ChainArgs p) {
   }
 }
 
+__device__ __forceinline__ float chain_load1(const ChainArgs& p, int l, int64_t off) {
+  return p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[off] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + off);
+}
+
 // one element per thread-iteration, any strides
+template <int NL>
 __global__ void __launch_bounds__(256) ew_chain1(ChainArgs p) {
   const uint32_t step = gridDim.x * blockDim.x;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += step) {
-    int64_t off[kChainLeaves];
-    chain_offsets(p, e, off);
-    float x[kChainLeaves];
-#pragma unroll
-    for (int l = 0; l < kChainLeaves; ++l) {
-      if (l < p.nleaves)
-        x[l] = p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[off[l]] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + off[l]);
-    }
-    float v = p.head_kind == 0 ? x[0] : p.head_scalar;
+    int64_t off[NL];
+    chain_offsets<NL>(p, e, off);
+    float x0 = chain_load1(p, 0, off[0]);
+    float x1 = NL > 1 ? chain_load1(p, 1, off[NL > 1 ? 1 : 0]) : 0.f;
+    float x2 = NL > 2 ? chain_load1(p, 2, off[NL > 2 ? 2 : 0]) : 0.f;
+    float x3 = NL > 3 ? chain_load1(p, 3, off[NL > 3 ? 3 : 0]) : 0.f;
+    float x4 = NL > 4 ? chain_load1(p, 4, off[NL > 4 ? 4 : 0]) : 0.f;
+    float x5 = NL > 5 ? chain_load1(p, 5, off[NL > 5 ? 5 : 0]) : 0.f;
+    float x6 = NL > 6 ? chain_load1(p, 6, off[NL > 6 ? 6 : 0]) : 0.f;
+    float x7 = NL > 7 ? chain_load1(p, 7, off[NL > 7 ? 7 : 0]) : 0.f;
+    float v = p.head_kind == 0 ? x0 : p.head_scalar;
     for (int s = 0; s < p.nsteps; ++s) {
       const ChainStep st = p.step[s];
-      if (st.kind == 0) {
-        v = chain_un(st.op - 64, st.to_bool, v);
-        continue;
-      }
-      float o;
-      if (st.kind == 1) {
-        o = x[0];
-#pragma unroll
-        for (int l = 1; l < kChainLeaves; ++l)
-          if (st.leaf == l) o = x[l];
-      } else {
-        o = st.kind == 2 ? st.scalar : v;
-      }
-      v = st.side == 0 ? chain_bin(st.op, v, o) : chain_bin(st.op, o, v);
+      float o = v;
+      if (st.kind == 1) o = pick<NL>(st.leaf, x0, x1, x2, x3, x4, x5, x6, x7);
+      else if (st.kind == 2) o = st.scalar;
+      float4 r = chain_step4(st, make_float4(v, v, v, v), make_float4(o, o, o, o));
+      v = r.x;
     }
     if (p.out_bool)
       ((uint8_t*)p.out)[e] = v != 0.f;
     else
       ((float*)p.out)[e] = v;
   }
+}
+
+template <int NL>
+static void launch_chain(ChainArgs& p, bool v4, cudaStream_t s) {
+  if (v4) ew_chain4<NL><<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
+  else ew_chain1<NL><<<grid_for(p.n, 256, 4), 256, 0, s>>>(p);
 }
 
 // ----------------------------------------------------------------------- host helpers
@@ -1037,11 +1070,19 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
   cudaStream_t s = compute_stream();
   if (v4) {
     p.n = (uint32_t)(n / 4);
-    ew_chain4<<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
   } else {
     for (int l = 0; l < kChainLeaves; ++l) p.vec[l] = 0;
     p.n = (uint32_t)n;
-    ew_chain1<<<grid_for(p.n, 256, 4), 256, 0, s>>>(p);
+  }
+  switch (nleaves) {
+    case 0: case 1: launch_chain<1>(p, v4, s); break;
+    case 2: launch_chain<2>(p, v4, s); break;
+    case 3: launch_chain<3>(p, v4, s); break;
+    case 4: launch_chain<4>(p, v4, s); break;
+    case 5: launch_chain<5>(p, v4, s); break;
+    case 6: launch_chain<6>(p, v4, s); break;
+    case 7: launch_chain<7>(p, v4, s); break;
+    default: launch_chain<8>(p, v4, s); break;
   }
   PB_LAUNCHED();
   return PB_OK;
