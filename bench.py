@@ -296,7 +296,7 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) images)",
             "config": cfg, "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
             "roofline": roofline, "clocks": clk.summary(), "final_loss": final_loss,
-            "gemm_path": "tcgen05" if be._lib.pb_gemm_path() else "simt",
+            "gemm_path": {2: "tcgen05+tma", 1: "tcgen05", 0: "simt"}[be._lib.pb_gemm_path()],
             "step_mode": "cuda_graph" if step is not None else "eager", "eager": eager}
     if graph_error:
         line["graph_error"] = graph_error

@@ -153,8 +153,8 @@ int pb_nccl_wait(void* comm);  /* compute stream waits for everything enqueued o
 
 /* ---- introspection ------------------------------------------------------------------ */
 uint64_t pb_launch_count(void);  /* kernels launched by this library so far */
-int pb_gemm_path(void);          /* 1 when the tcgen05 path is enabled, 0 = SIMT */
-int pb_set_gemm_path(int tc);
+int pb_gemm_path(void);          /* 2: tcgen05 with TMA-fed convs (default), 1: SIMT-fed tcgen05 only, 0: SIMT */
+int pb_set_gemm_path(int path);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
           "-Xptxas", "-O3", "--expt-relaxed-constexpr", "-I" + os.path.join(PKG, "..", "include")]
 NO_FMA = {"elementwise.cu", "reduce.cu", "rng.cu", "runtime.cu", "allocator.cu"}
 SOURCES = ["runtime.cu", "allocator.cu", "elementwise.cu", "reduce.cu", "rng.cu", "gemm_simt.cu",
-           "gemm_tc.cu", "contract.cu", "nccl.cu"]
+           "gemm_tc.cu", "gemm_tma.cu", "contract.cu", "nccl.cu"]
 
 
 def _obj(src):
@@ -30,7 +30,8 @@ def _obj(src):
 def _compile(src):
     s = os.path.join(HERE, src)
     o = _obj(src)
-    deps = [s, os.path.join(HERE, "common.cuh"), os.path.join(PKG, "..", "include", "paper_b200.h")]
+    deps = [s, os.path.join(PKG, "..", "include", "paper_b200.h")] + [
+        os.path.join(HERE, h) for h in os.listdir(HERE) if h.endswith(".cuh")]
     if os.path.exists(o) and all(os.path.getmtime(o) >= os.path.getmtime(d) for d in deps):
         return src, ""
     flags = COMMON + (["-fmad=false"] if src in NO_FMA else [])

@@ -1,6 +1,7 @@
-// Contraction dispatch: f32 x f32 matmul / conv go to the tcgen05 3xTF32 kernels
-// (gemm_tc.cu) when that path is enabled and the shape is supported; everything else
-// (f64, integer, mixed dtypes, unsupported shapes) runs the SIMT kernels (gemm_simt.cu).
+// Contraction dispatch.  Path 2 (default): f32 convs whose channel counts are multiples of 32
+// go to the TMA-fed tcgen05 3xTF32 kernels (gemm_tma.cu); path >= 1: other f32 matmul / conv
+// shapes go to the SIMT-fed tcgen05 kernels (gemm_tc.cu); everything else (f64, integer,
+// mixed dtypes, unsupported shapes) and path 0 run the SIMT kernels (gemm_simt.cu).
 #include "common.cuh"
 
 extern "C" {
@@ -13,15 +14,19 @@ int pb_matmul_tc(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out);
 int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_input_tc(const pb_tensor* g, const pb_tensor* w, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_weight_tc(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
+int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p, const pb_tensor* out);
+int pb_conv2d_grad_input_tma(const pb_tensor* g, const pb_tensor* w, const pb_conv* p, const pb_tensor* out);
+int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
 }
 
-static int g_tc = 1;
+static int g_tc = 2;
 
 extern "C" {
 
 int pb_gemm_path(void) { return g_tc; }
-int pb_set_gemm_path(int tc) {
-  g_tc = tc ? 1 : 0;
+int pb_set_gemm_path(int path) {
+  if (path < 0 || path > 2) return PB_ERR_ARG;
+  g_tc = path;
   return PB_OK;
 }
 
@@ -34,6 +39,10 @@ int pb_matmul(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
 }
 
 int pb_conv2d(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p, const pb_tensor* out) {
+  if (g_tc == 2) {
+    int rc = pb_conv2d_tma(x, w, bias, p, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
+  }
   if (g_tc) {
     int rc = pb_conv2d_tc(x, w, bias, p, out);
     if (rc != PB_ERR_UNSUPPORTED) return rc;
@@ -42,6 +51,10 @@ int pb_conv2d(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, con
 }
 
 int pb_conv2d_grad_input(const pb_tensor* g, const pb_tensor* w, const pb_conv* p, const pb_tensor* out) {
+  if (g_tc == 2) {
+    int rc = pb_conv2d_grad_input_tma(g, w, p, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
+  }
   if (g_tc) {
     int rc = pb_conv2d_grad_input_tc(g, w, p, out);
     if (rc != PB_ERR_UNSUPPORTED) return rc;
@@ -50,6 +63,10 @@ int pb_conv2d_grad_input(const pb_tensor* g, const pb_tensor* w, const pb_conv* 
 }
 
 int pb_conv2d_grad_weight(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out) {
+  if (g_tc == 2) {
+    int rc = pb_conv2d_grad_weight_tma(x, g, p, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
+  }
   if (g_tc) {
     int rc = pb_conv2d_grad_weight_tc(x, g, p, out);
     if (rc != PB_ERR_UNSUPPORTED) return rc;

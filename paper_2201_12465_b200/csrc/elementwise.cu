@@ -857,6 +857,35 @@ __global__ void __launch_bounds__(256) pad_fast(PadFast p, uint32_t value) {
   }
 }
 
+// innermost output extent % 4 == 0: one index decomposition per 4 consecutive outputs of a
+// row, 16-byte stores
+__global__ void __launch_bounds__(256) pad_fast4(PadFast p, uint32_t value) {
+  const uint32_t n4 = p.n >> 2;
+  const int in = p.nd - 1;
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
+    uint32_t e = q << 2, qq, x;
+    p.ext[in].divmod(e, qq, x);
+    int64_t so = 0;
+    bool inside = true;
+    e = qq;
+    for (int k = in - 1; k >= 0; --k) {
+      uint32_t q2, r;
+      p.ext[k].divmod(e, q2, r);
+      int j = (int)r - p.lo[k];
+      inside = inside && j >= 0 && j < p.sext[k];
+      so += (int64_t)j * p.sstr[k];
+      e = q2;
+    }
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = (int)x + u - p.lo[in];
+      v[u] = (inside && j >= 0 && j < p.sext[in]) ? __ldg(p.src + so + (int64_t)j * p.sstr[in]) : value;
+    }
+    reinterpret_cast<uint4*>(p.out)[q] = make_uint4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) fill_kernel(T* out, int64_t n, T v) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1132,7 +1161,10 @@ static bool pad_fast_path(const pb_tensor* src, const int64_t* lo, const pb_scal
     int32_t i = scalar_as<int32_t>(value);
     memcpy(&bits, &i, 4);
   }
-  pad_fast<<<grid_for(n, 1024), 256, 0, compute_stream()>>>(p, bits);
+  if (nd > 0 && oext[nd - 1] % 4 == 0 && out->ptr % 16 == 0)
+    pad_fast4<<<grid_for(n / 4, 256), 256, 0, compute_stream()>>>(p, bits);
+  else
+    pad_fast<<<grid_for(n, 1024), 256, 0, compute_stream()>>>(p, bits);
   count_launch();
   cudaError_t e = cudaGetLastError();
   *rc = e == cudaSuccess ? PB_OK : cuda_fail(e, "pb_pad");

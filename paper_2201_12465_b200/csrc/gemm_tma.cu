@@ -1,0 +1,752 @@
+// TMA-fed tcgen05 3xTF32 implicit-GEMM convolutions (minml/kernels.py:197-239):
+// conv2d fprop, stride-1 grad_input (dgrad) and stride-1 grad_weight (wgrad).
+//
+// gemm_tc.cu feeds the tensor cores from SIMT producer warps that gather, split and swizzle
+// every operand element; ncu shows those producers issue-bound at ~20 instructions per
+// element with the tensor pipe <10% busy.  Here the split moves out of the GEMM:
+//   1. a pre-pass (HBM-bound) writes each operand as two planes, hi = rna_tf32(x) and
+//      lo = x - hi (exact in f32): activations NHWC for fprop/dgrad; for wgrad x and g as
+//      per-(n, channel) planes on the zero-padded grid of row pitch Wp = roundup(W+2p, 4),
+//      flattened, so a filter tap (r, s) is a constant shift r*Wp + s along the plane (x is
+//      written once per s, pre-shifted by s, because TMA box starts must be 16-byte aligned);
+//      weights K-major [rows][(r,s,c)];
+//   2. the GEMM kernel's single producer thread loads every tile with TMA straight into
+//      128B-swizzled K-major shared memory: fprop/dgrad activation tiles in im2col mode (the
+//      hardware walks output pixels across rows and images, applies stride and padding and
+//      zero-fills out-of-range taps), weight tiles in tiled mode; wgrad tiles (K = positions
+//      on the padded output grid, 32 per k-block) as 3-D boxes of 32 positions x 128 channels,
+//      x shifted by r*Wp (copy s), g unshifted (g is zero on the padding columns);
+//   3. one thread issues 3 tcgen05.mma.kind::tf32 per 8-deep k step (lo*hi, hi*lo, hi*hi)
+//      into TMEM; the drain warps fold 2-k-block chunks into f32 registers with IEEE
+//      round-to-nearest (the same accumulation scheme as gemm_tc.cu, so results agree with it
+//      to rounding) and store through the output functor.
+// The split is gemm_tc.cu's (hi = rna_tf32(x), lo = rna_tf32(x - hi)), so both kernel
+// families produce the same products.
+//
+// Shapes the kernel declines (PB_ERR_UNSUPPORTED, no side effects) fall through to
+// gemm_tc.cu: channel counts not a multiple of 32 (the RGB stem), strided dgrad, and
+// anything whose coordinates do not fit the TMA limits.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include "common.cuh"
+#include "tc_common.cuh"
+
+namespace pb {
+namespace tma {
+
+using namespace pb::tc;
+
+constexpr int BM = 128;  // D rows per CTA = TMEM lanes
+constexpr int BK = 32;   // k per stage: one 128-byte swizzled row of f32
+constexpr int CK = 2;    // k-blocks accumulated in TMEM per register drain
+
+// ---- driver entry points (no libcuda link: resolved through the runtime) -------------------
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+typedef CUresult (*EncodeIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                 CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiled g_tiled = nullptr;
+static EncodeIm2col g_im2col = nullptr;
+
+static bool driver_ok() {
+  static int state = -1;
+  if (state < 0) {
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    state = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f1, cudaEnableDefault, &q1) == cudaSuccess &&
+            cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f2, cudaEnableDefault, &q2) == cudaSuccess &&
+            q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && f1 && f2;
+    g_tiled = (EncodeTiled)f1;
+    g_im2col = (EncodeIm2col)f2;
+  }
+  return state == 1;
+}
+
+// 2-D K-major (or MN-major) plane [rows][cols] f32, box {32 cols, box_rows}
+static bool map_2d(CUtensorMap* m, const float* p, int64_t cols, int64_t rows, int box_rows) {
+  cuuint64_t dim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t str[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return g_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)p, dim, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// flattened planes [copies][N][C][L] (L % 4 == 0), box {32 positions, bc channels, 1, 1}
+static bool map_planes(CUtensorMap* m, const float* p, int copies, int N, int C, int64_t L, int bc) {
+  cuuint64_t dim[4] = {(cuuint64_t)L, (cuuint64_t)C, (cuuint64_t)N, (cuuint64_t)copies};
+  cuuint64_t str[3] = {(cuuint64_t)L * 4, (cuuint64_t)C * L * 4, (cuuint64_t)N * C * L * 4};
+  cuuint32_t box[4] = {32, (cuuint32_t)bc, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)p, dim, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// NHWC plane [N][H][W][C] in im2col mode: 32 channels x `pixels` output pixels per load
+static bool map_im2col(CUtensorMap* m, const float* p, int N, int H, int W, int C, int KH, int KW, int SH, int SW,
+                       int PH, int PW, int pixels) {
+  cuuint64_t dim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t str[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  int lower[2] = {-PW, -PH};
+  int upper[2] = {PW - (KW - 1), PH - (KH - 1)};
+  cuuint32_t es[4] = {1, (cuuint32_t)SW, (cuuint32_t)SH, 1};
+  return g_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)p, dim, str, lower, upper, 32, (cuuint32_t)pixels,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// ---- PTX: TMA loads, expect-tx --------------------------------------------------------------
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(dst),
+      "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_im2col(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int c, int w, int h,
+                                           int n, uint16_t ow, uint16_t oh) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(dst),
+      "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int x, int y, int z,
+                                       int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(dst),
+      "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");
+}
+
+// UMMA smem descriptor, SWIZZLE_128B, K-major: SBO = 1024 B between 8-row groups
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: D f32, A/B tf32, K-major unless transposed (bit 15 A, bit 16 B)
+__host__ __device__ constexpr uint32_t idesc(int M, int N, bool mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (mn ? (1u << 15) | (1u << 16) : 0u) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// ---- problem descriptions --------------------------------------------------------------------
+// CONV (fprop, and stride-1 dgrad as an fprop over the gradient with flipped weights):
+//   D[i = (n,ho,wo)][j = f] = sum_{k = (r,s,c)} X[n, ho*sh-ph+r, wo*sw-pw+s, c] * Wt[f][k]
+// WGRAD (stride 1), q = ho * Wp + wo on the padded grid (Wp = roundup(W + 2pw, 4)):
+//   D[i = c][j = f] (tap z % RS, split z / RS) = sum_{n, q} Xs[s][n, c, q + r*Wp] * Gpad[n, f, q]
+//   with Xs[s][n, c, q] = Xpad[n, c, q + s]
+struct Prob {
+  int N, H, W, C;      // activation plane X (NHWC)
+  int KH, KW, SH, SW, PH, PW, HO, WO;
+  int F;               // output channels (fprop / wgrad), or input channels (dgrad)
+  int Mi, Nj, K;       // GEMM extents
+  int kper;            // wgrad: k per split (multiple of BK)
+  int Wp;              // wgrad: padded row pitch roundup(W + 2pw, 4)
+  FastDiv fKB;         // wgrad: k-blocks per image
+  int ti, tj, ntiles, zdim;
+  FastDiv fP, fWO;     // output pixel decode (ho*wo, wo)
+};
+
+template <int BN, bool WG>
+struct Cfg {
+  static constexpr int A_BYTES = BM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int STAGES = (200 * 1024) / STAGE;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static constexpr int NDRAIN = BN / 16;
+  static constexpr int THREADS = 64 + NDRAIN * 32;
+  static constexpr int TMEM_COLS = 4 * BN;
+  static constexpr uint32_t IDESC = idesc(BM, BN, false);
+};
+
+// Output functor for wgrad: tap-major columns into dw[f][c][r][s] (split 0) or the split-K
+// workspace ws[split][f][c][r][s]; folded afterwards by fold_partials with OutMat.
+// Output functor for strided 1x1 dgrad: row i = (n, ho, wo) of the gradient grid writes
+// dx[n][j][ho*s][wo*s]; the other pixels receive no contribution and are zero-filled first
+struct OutScatter {
+  float* p;
+  int Mi, Nj;
+  FastDiv fP, fWO;
+  int sh, sw, W, HW;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = nullptr;
+    if (i < Mi) {
+      uint32_t n, pix, ho, wo;
+      fP.divmod(i, n, pix);
+      fWO.divmod(pix, ho, wo);
+      o.p = p + (int64_t)n * Nj * HW + (int64_t)ho * sh * W + (int64_t)wo * sw;
+    }
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < Nj) rw.p[(int64_t)j * HW] = v;
+  }
+};
+
+struct OutWgrad {
+  float* p;
+  int C, F, RS;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int z, int i) const {
+    Row o;
+    const int split = z / RS, tap = z - split * RS;
+    o.p = i < C ? p + (int64_t)split * F * C * RS + (int64_t)i * RS + tap : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < F) rw.p[(int64_t)j * C * RS] = v;
+  }
+};
+
+template <int BN, bool WG, class OUT>
+__global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
+    tma_conv_kernel(const __grid_constant__ CUtensorMap xa_hi, const __grid_constant__ CUtensorMap xa_lo,
+                    const __grid_constant__ CUtensorMap b_hi, const __grid_constant__ CUtensorMap b_lo, Prob pr,
+                    OUT out) {
+  typedef Cfg<BN, WG> C;
+  extern __shared__ uint8_t smem_raw[];
+  char* smem = (char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* accf = empty + C::STAGES;
+  uint64_t* acce = accf + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int per_z = pr.ti * pr.tj;
+  const int cblocks = pr.C / BK;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&accf[s], 1);
+      mbar_init(&acce[s], C::NDRAIN * 32);
+    }
+    fence_barrier_init();
+    prefetch_map(&xa_hi);
+    prefetch_map(&xa_lo);
+    prefetch_map(&b_hi);
+    prefetch_map(&b_lo);
+  }
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // k range of tile t: CONV covers all of K; WGRAD's z = split * RS + tap takes one split
+  auto krange = [&](int t, int& kbeg, int& kend) {
+    if (WG) {
+      const int z = t / per_z, split = z / (pr.KH * pr.KW);
+      kbeg = split * pr.kper;
+      kend = min(pr.K, kbeg + pr.kper);
+    } else {
+      kbeg = 0;
+      kend = pr.K;
+    }
+  };
+
+  if (warp == 0) {
+    // ===== TMA producer (one thread) =====
+    if (tid == 0) {
+      uint32_t it = 0;
+      for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
+        const int z = t / per_z, rem = t - z * per_z;
+        const int i0 = (rem / pr.tj) * BM, j0 = (rem % pr.tj) * BN;
+        int kbeg, kend;
+        krange(t, kbeg, kend);
+        const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+        int n = 0, ho = 0, wo = 0, tr = 0, ts = 0;
+        if (!WG) {  // first output pixel of the tile
+          uint32_t nn, pix, h, w;
+          pr.fP.divmod((uint32_t)i0, nn, pix);
+          pr.fWO.divmod(pix, h, w);
+          n = (int)nn, ho = (int)h, wo = (int)w;
+        } else {
+          const int tap = z % (pr.KH * pr.KW);
+          tr = tap / pr.KW;
+          ts = tap - tr * pr.KW;
+        }
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          if (it >= (uint32_t)C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
+          const uint32_t base = smem_u32(smem + s * C::STAGE);
+          mbar_expect_tx(&full[s], C::STAGE);
+          const int k0 = kbeg + kb * BK;
+          if (!WG) {
+            const int tap = kb / cblocks, c0 = (kb - tap * cblocks) * BK;
+            const int r = tap / pr.KW, sx = tap - r * pr.KW;
+            const int wc = wo * pr.SW - pr.PW, hc = ho * pr.SH - pr.PH;
+            tma_im2col(base, &xa_hi, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
+            tma_im2col(base + C::A_BYTES, &xa_lo, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
+            tma_2d(base + 2 * C::A_BYTES, &b_hi, &full[s], k0, j0);
+            tma_2d(base + 2 * C::A_BYTES + C::B_BYTES, &b_lo, &full[s], k0, j0);
+          } else {
+            // k-block k0 / BK -> (image, 32 positions of its padded output grid)
+            uint32_t nn, qb;
+            pr.fKB.divmod((uint32_t)(k0 / BK), nn, qb);
+            const int q0 = (int)qb * BK, sh = tr * pr.Wp;
+            tma_4d(base, &xa_hi, &full[s], q0 + sh, i0, (int)nn, ts);
+            tma_4d(base + C::A_BYTES, &xa_lo, &full[s], q0 + sh, i0, (int)nn, ts);
+            tma_4d(base + 2 * C::A_BYTES, &b_hi, &full[s], q0, j0, (int)nn, 0);
+            tma_4d(base + 2 * C::A_BYTES + C::B_BYTES, &b_lo, &full[s], q0, j0, (int)nn, 0);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===== MMA issuer (one thread) =====
+    if ((tid & 31) == 0) {
+      uint32_t it = 0, cc = 0;
+      for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
+        int kbeg, kend;
+        krange(t, kbeg, kend);
+        const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+        uint32_t dbig = 0, dsmall = 0;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % C::STAGES;
+          const bool first = (kb % CK) == 0;
+          if (first) {
+            const uint32_t buf = cc & 1;
+            if (cc >= 2) {
+              mbar_wait(&acce[buf], ((cc >> 1) - 1) & 1);
+              tc_fence_after();
+            }
+            dbig = tmem + buf * 2 * BN;
+            dsmall = dbig + BN;
+          }
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          const uint32_t base = smem_u32(smem + s * C::STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk) {
+            const uint32_t adv = kk * 32;  // 8 tf32 along the 128-byte swizzled row
+            const uint64_t ahi = desc_kmajor(base + adv), alo = desc_kmajor(base + C::A_BYTES + adv);
+            const uint64_t bhi = desc_kmajor(base + 2 * C::A_BYTES + adv);
+            const uint64_t blo = desc_kmajor(base + 2 * C::A_BYTES + C::B_BYTES + adv);
+            const uint32_t acc = !(first && kk == 0);
+            mma_tf32(dsmall, alo, bhi, C::IDESC, acc);
+            mma_tf32(dsmall, ahi, blo, C::IDESC, 1);
+            mma_tf32(dbig, ahi, bhi, C::IDESC, acc);
+          }
+          mma_commit(&empty[s]);
+          if ((kb % CK) == CK - 1 || kb == nkb - 1) {
+            mma_commit(&accf[cc & 1]);
+            ++cc;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===== drain + epilogue: TMEM lane quadrant is fixed by warp % 4 =====
+    const int q = warp & 3, cg = (warp - 2) >> 2;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cg * 64);
+    uint32_t cc = 0;
+    for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
+      const int z = t / per_z, rem = t - z * per_z;
+      const int i0 = (rem / pr.tj) * BM, j0 = (rem % pr.tj) * BN;
+      int kbeg, kend;
+      krange(t, kbeg, kend);
+      const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+      float acc[64];
+#pragma unroll
+      for (int e = 0; e < 64; ++e) acc[e] = 0.f;
+      const int nch = (nkb + CK - 1) / CK;
+      for (int c = 0; c < nch; ++c, ++cc) {
+        const uint32_t buf = cc & 1;
+        mbar_wait(&accf[buf], (cc >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          uint32_t rb[16], rs[16];
+          tmem_ld16(lane_base + buf * 2 * BN + (uint32_t)(p * 16), rb);
+          tmem_ld16(lane_base + buf * 2 * BN + BN + (uint32_t)(p * 16), rs);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e)
+            acc[p * 16 + e] = __fadd_rn(acc[p * 16 + e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
+        }
+        tc_fence_before();
+        mbar_arrive(&acce[buf]);
+      }
+      const int i = i0 + q * 32 + (tid & 31);
+      typename OUT::Row orow = out.row(z, i);
+#pragma unroll
+      for (int e = 0; e < 64; ++e) out.put(orow, j0 + cg * 64 + e, acc[e]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc<C::TMEM_COLS>(tmem);
+  }
+}
+
+// ---- pre-pass kernels -----------------------------------------------------------------------
+// hi = rna_tf32(x), lo = rna_tf32(x - hi): the same split as gemm_tc.cu's producers (free
+// here: the pre-pass is HBM-bound), |lo| <= 2^-11 |x|, per-product error <= ~2^-22
+__device__ __forceinline__ void split_hl(float x, float& h, float& l) {
+  split1(x, h, l);
+}
+
+// x[n][c][p] (NCHW, C % 32 == 0) -> hi/lo[n][p][c] (NHWC), a 32x32 tile per block through smem
+__global__ void __launch_bounds__(256) nchw_split_nhwc(const float* __restrict__ x, float* __restrict__ hi,
+                                                       float* __restrict__ lo, int C, int P) {
+  __shared__ float t[32][33];
+  const int n = blockIdx.z, c0 = blockIdx.y * 32, p0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const float* src = x + ((int64_t)n * C + c0) * P + p0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = ty + 8 * k;
+    t[c][tx] = p0 + tx < P ? __ldg(src + (int64_t)c * P + tx) : 0.f;
+  }
+  __syncthreads();
+  const int64_t ob = ((int64_t)n * P + p0) * C + c0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int p = ty + 8 * k;
+    if (p0 + p < P) {
+      float h, l;
+      split_hl(t[tx][p], h, l);
+      hi[ob + (int64_t)p * C + tx] = h;
+      lo[ob + (int64_t)p * C + tx] = l;
+    }
+  }
+}
+
+// x[plane][H][W] -> hi/lo[copy][plane][L] for copy = 0..copies-1: position q of copy j holds
+// x[hq - off][wq - off] with hq * Wp + wq = q + j (zero outside the image), L % 4 == 0
+__global__ void __launch_bounds__(256) split_planes(const float* __restrict__ x, float* __restrict__ hi,
+                                                    float* __restrict__ lo, int64_t n, int copies, FastDiv fL,
+                                                    FastDiv fWp, int H, int W, int off) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t plane, q;
+    fL.divmod((uint32_t)i, plane, q);
+    for (int j = 0; j < copies; ++j) {
+      uint32_t hq, wq;
+      fWp.divmod(q + j, hq, wq);
+      const int hh = (int)hq - off, ww = (int)wq - off;
+      float h = 0.f, l = 0.f;
+      if ((unsigned)hh < (unsigned)H && (unsigned)ww < (unsigned)W)
+        split_hl(__ldg(x + ((int64_t)plane * H + hh) * W + ww), h, l);
+      hi[i + j * n] = h;
+      lo[i + j * n] = l;
+    }
+  }
+}
+
+// weights w[f][c][r][s] -> hi/lo[a][(r,s,b)]: fprop (a,b) = (f,c); dgrad (a,b) = (c,f) with the
+// taps flipped (r,s) -> (KH-1-r, KW-1-s)
+__global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int F,
+                             int Cc, int KH, int KW, int dgrad) {
+  const int RS = KH * KW;
+  const int64_t n = (int64_t)F * Cc * RS;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int rs = (int)(idx % RS);
+    const int64_t t = idx / RS;
+    const int c = (int)(t % Cc), f = (int)(t / Cc);
+    float h, l;
+    split_hl(w[idx], h, l);
+    int64_t d;
+    if (!dgrad) {
+      d = ((int64_t)f * RS + rs) * Cc + c;
+    } else {
+      const int r = rs / KW, s = rs - r * KW;
+      const int fr = (KH - 1 - r) * KW + (KW - 1 - s);
+      d = ((int64_t)c * RS + fr) * F + f;
+    }
+    hi[d] = h;
+    lo[d] = l;
+  }
+}
+
+// ---- host ----------------------------------------------------------------------------------
+template <int BN, bool WG, class OUT>
+static int launch(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMap& bh, const CUtensorMap& bl,
+                  Prob& pr, const OUT& out) {
+  typedef Cfg<BN, WG> C;
+  static bool attr = false;
+  if (!attr) {
+    PB_CUDA(cudaFuncSetAttribute(tma_conv_kernel<BN, WG, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    attr = true;
+  }
+  pr.ti = (pr.Mi + BM - 1) / BM;
+  pr.tj = (pr.Nj + BN - 1) / BN;
+  const int64_t nt = (int64_t)pr.ti * pr.tj * pr.zdim;
+  if (nt >= ((int64_t)1 << 31)) return PB_ERR_UNSUPPORTED;
+  pr.ntiles = (int)nt;
+  const int grid = (int)(nt < num_sms() ? nt : num_sms());
+  tma_conv_kernel<BN, WG, OUT><<<grid, C::THREADS, C::SMEM, compute_stream()>>>(ah, al, bh, bl, pr, out);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+static int split_act(const float* x, float* hi, float* lo, int N, int C, int P) {
+  dim3 grid((P + 31) / 32, C / 32, N);
+  nchw_split_nhwc<<<grid, 256, 0, compute_stream()>>>(x, hi, lo, C, P);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+static bool fits(int64_t v) { return v < ((int64_t)1 << 31) - 1024; }
+
+static Prob make_prob(int N, int H, int W, int C, int KH, int KW, int SH, int SW, int PH, int PW) {
+  Prob pr{};
+  pr.N = N, pr.H = H, pr.W = W, pr.C = C, pr.KH = KH, pr.KW = KW, pr.SH = SH, pr.SW = SW, pr.PH = PH, pr.PW = PW;
+  pr.HO = (H + 2 * PH - KH) / SH + 1;
+  pr.WO = (W + 2 * PW - KW) / SW + 1;
+  pr.fP = FastDiv((uint32_t)(pr.HO * pr.WO));
+  pr.fWO = FastDiv((uint32_t)pr.WO);
+  return pr;
+}
+
+// D = implicit GEMM over the NHWC planes (xh, xl) and K-major weight planes (wh, wl) [Nj][K]
+template <class OUT>
+static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh, const float* wl, const OUT& o) {
+  CUtensorMap ah, al, bh, bl;
+  const int BN = pr.Nj <= 64 ? 64 : 128;  // (128-wide tiles win even with a ragged last wave)
+  if (!map_im2col(&ah, xh, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM) ||
+      !map_im2col(&al, xl, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM) ||
+      !map_2d(&bh, wh, pr.K, pr.Nj, BN) || !map_2d(&bl, wl, pr.K, pr.Nj, BN))
+    return fail(PB_ERR_CUDA, "tma conv: tensor map encoding failed");
+  pr.zdim = 1;
+  if (BN == 64) return launch<64, false>(ah, al, bh, bl, pr, o);
+  return launch<128, false>(ah, al, bh, bl, pr, o);
+}
+
+static bool geometry_ok(const Prob& pr) {
+  // im2col corners and 16-bit tap offsets; the C % 32 channel blocks; i32 indexing
+  return pr.C % 32 == 0 && pr.KH <= 32 && pr.KW <= 32 && pr.PH <= 64 && pr.PW <= 64 && pr.HO > 0 && pr.WO > 0 &&
+         pr.SH <= 8 && pr.SW <= 8;
+}
+
+}  // namespace tma
+}  // namespace pb
+
+using namespace pb;
+using namespace pb::tma;
+
+static int g_tma = 1;
+
+extern "C" {
+
+int pb_tma_enable(int on) {
+  g_tma = on ? 1 : 0;
+  return PB_OK;
+}
+int pb_tma_enabled(void) { return g_tma && driver_ok(); }
+
+int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p,
+                  const pb_tensor* out) {
+  if (!g_tma || !driver_ok()) return PB_ERR_UNSUPPORTED;
+  if (x->dtype != PB_F32 || w->dtype != PB_F32 || out->dtype != PB_F32 || (bias && bias->dtype != PB_F32))
+    return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*x) || !is_contiguous(*w) || !is_contiguous(*out)) return PB_ERR_UNSUPPORTED;
+  const int N = (int)x->shape[0], C = (int)x->shape[1], H = (int)x->shape[2], W = (int)x->shape[3];
+  const int F = (int)w->shape[0], KH = (int)w->shape[2], KW = (int)w->shape[3];
+  Prob pr = make_prob(N, H, W, C, KH, KW, p->stride_h, p->stride_w, p->pad_h, p->pad_w);
+  if (!geometry_ok(pr) || F == 0 || N == 0) return PB_ERR_UNSUPPORTED;
+  const int64_t act = (int64_t)N * C * H * W, K = (int64_t)C * KH * KW, rows = (int64_t)N * pr.HO * pr.WO;
+  if (!fits(act) || !fits(rows * F) || !fits(K * F) || F % 4 != 0) return PB_ERR_UNSUPPORTED;
+  pr.F = F;
+  pr.Mi = (int)rows;
+  pr.Nj = F;
+  pr.K = (int)K;
+  const size_t wb = ((size_t)F * K * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
+  char* ws = (char*)workspace(2 * wb + 2 * ab);
+  if (!ws) return fail(PB_ERR_OOM, "conv2d (tma): no workspace");
+  float *wh = (float*)ws, *wl = (float*)(ws + wb), *xh = (float*)(ws + 2 * wb), *xl = (float*)(ws + 2 * wb + ab);
+  weight_split<<<grid_for((int64_t)F * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F,
+                                                                            C, KH, KW, 0);
+  PB_LAUNCHED();
+  int rc = split_act((const float*)(uintptr_t)x->ptr, xh, xl, N, C, H * W);
+  if (rc) return rc;
+  OutConv o{(float*)(uintptr_t)out->ptr, bias ? (const float*)(uintptr_t)bias->ptr : nullptr, (int)rows, F,
+            FastDiv((uint32_t)(pr.HO * pr.WO))};
+  return run_conv(pr, xh, xl, wh, wl, o);
+}
+
+// stride-1 dgrad: dx = conv(g, flip(w)^T) with padding KH-1-ph
+int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_conv* p, const pb_tensor* out) {
+  if (!g_tma || !driver_ok()) return PB_ERR_UNSUPPORTED;
+  if (gr->dtype != PB_F32 || w->dtype != PB_F32 || out->dtype != PB_F32) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*gr) || !is_contiguous(*w) || !is_contiguous(*out)) return PB_ERR_UNSUPPORTED;
+  const int N = (int)out->shape[0], Cx = (int)out->shape[1], H = (int)out->shape[2], W = (int)out->shape[3];
+  const int F = (int)w->shape[0], KH = (int)w->shape[2], KW = (int)w->shape[3];
+  const int HO = (int)gr->shape[2], WO = (int)gr->shape[3];
+  if ((p->stride_h != 1 || p->stride_w != 1) && KH == 1 && KW == 1 && p->pad_h == 0 && p->pad_w == 0) {
+    // strided 1x1: dx[n, :, ho*s, wo*s] = W^T g[n, :, ho, wo], zero elsewhere
+    Prob pr = make_prob(N, HO, WO, F, 1, 1, 1, 1, 0, 0);
+    const int64_t act = (int64_t)N * F * HO * WO, rows = (int64_t)N * HO * WO;
+    if (!geometry_ok(pr) || Cx == 0 || N == 0 || !fits(act) || !fits((int64_t)N * Cx * H * W) || !fits((int64_t)F * Cx))
+      return PB_ERR_UNSUPPORTED;
+    pr.F = Cx;
+    pr.Mi = (int)rows;
+    pr.Nj = Cx;
+    pr.K = F;
+    const size_t wb = ((size_t)Cx * F * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
+    char* ws = (char*)workspace(2 * wb + 2 * ab);
+    if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
+    float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
+    PB_CUDA(cudaMemsetAsync((void*)(uintptr_t)out->ptr, 0, (size_t)N * Cx * H * W * 4, compute_stream()));
+    weight_split<<<grid_for((int64_t)Cx * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl,
+                                                                               F, Cx, 1, 1, 1);
+    PB_LAUNCHED();
+    int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
+    if (rc) return rc;
+    OutScatter o{(float*)(uintptr_t)out->ptr, (int)rows, Cx, FastDiv((uint32_t)(HO * WO)), FastDiv((uint32_t)WO),
+                 p->stride_h, p->stride_w, W, H * W};
+    return run_conv(pr, gh, gl, wh, wl, o);
+  }
+  if (p->stride_h != 1 || p->stride_w != 1) return PB_ERR_UNSUPPORTED;
+  const int ph = KH - 1 - p->pad_h, pw = KW - 1 - p->pad_w;
+  if (ph < 0 || pw < 0) return PB_ERR_UNSUPPORTED;
+  // the "conv" runs over g [N, F, HO, WO] and produces [N, Cx, H, W]
+  Prob pr = make_prob(N, HO, WO, F, KH, KW, 1, 1, ph, pw);
+  if (!geometry_ok(pr) || pr.HO != H || pr.WO != W || Cx == 0 || N == 0 || Cx % 4 != 0) return PB_ERR_UNSUPPORTED;
+  const int64_t act = (int64_t)N * F * HO * WO, K = (int64_t)F * KH * KW, rows = (int64_t)N * H * W;
+  if (!fits(act) || !fits(rows * Cx) || !fits(K * Cx)) return PB_ERR_UNSUPPORTED;
+  pr.F = Cx;
+  pr.Mi = (int)rows;
+  pr.Nj = Cx;
+  pr.K = (int)K;
+  const size_t wb = ((size_t)Cx * K * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
+  char* ws = (char*)workspace(2 * wb + 2 * ab);
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
+  float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
+  weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl,
+                                                                             F, Cx, KH, KW, 1);
+  PB_LAUNCHED();
+  int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
+  if (rc) return rc;
+  OutConv o{(float*)(uintptr_t)out->ptr, nullptr, (int)rows, Cx, FastDiv((uint32_t)(H * W))};
+  return run_conv(pr, gh, gl, wh, wl, o);
+}
+
+// stride-1 wgrad over the padded output grid (see the header): K = N * ceil(HO*Wp / 32) * 32
+int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* gr, const pb_conv* p, const pb_tensor* out) {
+  static int off = -1;  // experiment hook: PB_TMA_WGRAD=0 sends wgrad to gemm_tc.cu
+  if (off < 0) {
+    const char* e = getenv("PB_TMA_WGRAD");
+    off = e && e[0] == '0';
+  }
+  if (!g_tma || off || !driver_ok()) return PB_ERR_UNSUPPORTED;
+  if (x->dtype != PB_F32 || gr->dtype != PB_F32 || out->dtype != PB_F32) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*x) || !is_contiguous(*gr) || !is_contiguous(*out)) return PB_ERR_UNSUPPORTED;
+  if (p->stride_h != 1 || p->stride_w != 1 || p->pad_h != p->pad_w) return PB_ERR_UNSUPPORTED;
+  const int N = (int)x->shape[0], C = (int)x->shape[1], H = (int)x->shape[2], W = (int)x->shape[3];
+  const int F = (int)out->shape[0], KH = (int)out->shape[2], KW = (int)out->shape[3];
+  Prob pr = make_prob(N, H, W, C, KH, KW, 1, 1, p->pad_h, p->pad_w);
+  if (pr.HO <= 0 || pr.WO <= 0 || N == 0 || C == 0 || F == 0) return PB_ERR_UNSUPPORTED;
+  const int HO = pr.HO, RS = KH * KW, pad = p->pad_h;
+  {
+    // Measured on B200 (tools/conv_table.py): the plane pre-pass and the hi/lo operand stream
+    // cost more than they save on large pixel counts, where gemm_tc.cu's SIMT-fed wgrad wins;
+    // take the TMA kernel for small planes, 3x3 taps up to 28x28 at b32, and wide 1x1 convs.
+    static int force = -1;  // experiment hook: PB_TMA_WGRAD=2 takes every eligible shape
+    if (force < 0) {
+      const char* e = getenv("PB_TMA_WGRAD");
+      force = e && e[0] == '2';
+    }
+    const int64_t P = (int64_t)N * HO * pr.WO;
+    const bool win = P <= 6272 || (P <= 25088 && (RS > 1 || (int64_t)C * F >= 131072));
+    if (!force && !win) return PB_ERR_UNSUPPORTED;
+  }
+  pr.Wp = (W + 2 * pad + 3) / 4 * 4;
+  const int64_t Hp = H + 2 * pad;
+  const int64_t Lx = (Hp * pr.Wp + 3) / 4 * 4, Lg = ((int64_t)HO * pr.Wp + 3) / 4 * 4;
+  const int64_t kb_img = ((int64_t)HO * pr.Wp + BK - 1) / BK, KB = (int64_t)N * kb_img;
+  const int64_t xs = (int64_t)N * C * Lx, gs = (int64_t)N * F * Lg;
+  if (!fits(xs * KW) || !fits(gs) || !fits(KB * BK) || !fits((int64_t)F * C * RS) || (int64_t)(KH - 1) * pr.Wp + KW > 65535)
+    return PB_ERR_UNSUPPORTED;
+  pr.fKB = FastDiv((uint32_t)kb_img);
+  pr.F = F;
+  pr.Mi = C;
+  pr.Nj = F;
+  pr.K = (int)(KB * BK);
+  const int BN = F <= 64 ? 64 : 128;
+  // split K so that tiles x splits fill the machine; k per split a multiple of BK
+  const int64_t tiles = (int64_t)((C + BM - 1) / BM) * ((F + BN - 1) / BN) * RS;
+  int splits = 1;
+  if (tiles < num_sms()) {
+    splits = (int)(num_sms() / tiles);  // whole waves: one more tile than the SM count costs a wave
+    const int maxs = (int)(KB / 4);
+    if (splits > maxs) splits = maxs;
+    if (splits < 1) splits = 1;
+  }
+  {
+    const char* e = getenv("PB_TMA_WG_SPLITS");  // experiment hook
+    if (e && atoi(e) > 0) splits = atoi(e);
+  }
+  int per = (int)((pr.K + splits - 1) / splits);
+  per = (per + BK - 1) / BK * BK;
+  splits = (pr.K + per - 1) / per;
+  pr.kper = per;
+  pr.zdim = splits * RS;
+  const size_t ab = ((size_t)xs * KW * 4 + 1023) / 1024 * 1024, gb = ((size_t)gs * 4 + 1023) / 1024 * 1024;
+  const size_t pb = splits > 1 ? (size_t)splits * F * C * RS * 4 : 0;
+  char* ws = (char*)workspace(2 * ab + 2 * gb + pb);
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_weight (tma): no workspace");
+  float *xh = (float*)ws, *xl = (float*)(ws + ab), *gh = (float*)(ws + 2 * ab), *gl = (float*)(ws + 2 * ab + gb);
+  float* part = (float*)(ws + 2 * ab + 2 * gb);
+  split_planes<<<grid_for(xs, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)x->ptr, xh, xl, xs, KW,
+                                                                 FastDiv((uint32_t)Lx), FastDiv((uint32_t)pr.Wp), H,
+                                                                 W, pad);
+  PB_LAUNCHED();
+  split_planes<<<grid_for(gs, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)gr->ptr, gh, gl, gs, 1,
+                                                                 FastDiv((uint32_t)Lg), FastDiv((uint32_t)pr.Wp), HO,
+                                                                 pr.WO, 0);
+  PB_LAUNCHED();
+  CUtensorMap ah, al, bh, bl;
+  if (!map_planes(&ah, xh, KW, N, C, Lx, BM) || !map_planes(&al, xl, KW, N, C, Lx, BM) ||
+      !map_planes(&bh, gh, 1, N, F, Lg, BN) || !map_planes(&bl, gl, 1, N, F, Lg, BN))
+    return fail(PB_ERR_CUDA, "wgrad (tma): tensor map encoding failed");
+  float* dw = (float*)(uintptr_t)out->ptr;
+  OutWgrad o{splits > 1 ? part : dw, C, F, RS};
+  int rc = BN == 64 ? launch<64, true>(ah, al, bh, bl, pr, o) : launch<128, true>(ah, al, bh, bl, pr, o);
+  if (rc || splits == 1) return rc;
+  OutMat fin{dw, C * RS, F, (int64_t)C * RS, 0};
+  fold_partials<OutMat><<<grid_for((int64_t)C * RS * F, 256), 256, 0, compute_stream()>>>(part, splits, C * RS, F, fin);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+}  // extern "C"

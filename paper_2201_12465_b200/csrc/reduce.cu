@@ -88,20 +88,59 @@ struct RedArgs {
   void* out;      // final output (chunks == 1) — typed by `dto`
   void* partial;  // [chunks][O] accumulators (chunks > 1)
   int dto;
-  int nd;                        // outer (kept) dims
+  int nd;                        // outer (kept) dims, adjacent ones merged when contiguous
+  int fast;                      // O < 2^31: decode outputs with 32-bit FastDiv
   int64_t shape[PB_MAX_RANK];    // kept dims, row-major over outputs
   int64_t st[PB_MAX_RANK];       // their strides in a
+  FastDiv fd[PB_MAX_RANK];
   int64_t O, R, sR, chunk, chunks;
 };
 
 __device__ __forceinline__ int64_t out_base(const RedArgs& r, int64_t o) {
   int64_t off = 0;
+  if (r.fast) {
+    uint32_t q = (uint32_t)o;
+    for (int k = r.nd - 1; k > 0; --k) {
+      uint32_t nq, idx;
+      r.fd[k].divmod(q, nq, idx);
+      off += (int64_t)idx * r.st[k];
+      q = nq;
+    }
+    return r.nd > 0 ? off + (int64_t)q * r.st[0] : 0;
+  }
   for (int k = r.nd - 1; k >= 0; --k) {
     int64_t idx = o % r.shape[k];
     o /= r.shape[k];
     off += idx * r.st[k];
   }
   return off;
+}
+
+// fold lane (lane + s)'s accumulator into lane's, for lanes covering [lane, lane + 2s) of an
+// interleaved walk: sums add, extrema take the better value with ties (and NaNs) going to the
+// lower index, so the result equals a sequential first-wins walk
+template <int OP, typename T>
+__device__ __forceinline__ void lane_fold(typename Red<OP, T>::Acc& acc, int lane, int s, unsigned mask) {
+  typedef Red<OP, T> RD;
+  typename RD::Acc other;
+  other.v = __shfl_sync(mask, acc.v, (lane + s) & 31);
+  other.i = OP == PB_SUM ? 0 : __shfl_sync(mask, acc.i, (lane + s) & 31);
+  if ((lane & (2 * s - 1)) != 0) return;
+  if (OP == PB_SUM) {
+    acc = RD::merge(acc, other);
+    return;
+  }
+  if (other.i < 0) return;
+  if (acc.i < 0) {
+    acc = other;
+    return;
+  }
+  bool an = nan_(acc.v), bn = nan_(other.v);
+  bool take;
+  if (an || bn) take = bn && (!an || other.i < acc.i);
+  else if (OP == PB_RMAX || OP == PB_ARGMAX) take = other.v > acc.v || (other.v == acc.v && other.i < acc.i);
+  else take = other.v < acc.v || (other.v == acc.v && other.i < acc.i);
+  if (take) acc = other;
 }
 
 template <int OP, typename T>
@@ -135,34 +174,12 @@ __global__ void __launch_bounds__(256) red_warp(RedArgs r) {
     for (int64_t j = r0 + lane; j < r1; j += 32) RD::add(acc, a[base + j * r.sR], j);
     // lanes hold interleaved indices; fold in lane order so ties keep the lowest index
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      Acc other;
-      other.v = shfl(acc.v, (lane + s) & 31);
-      other.i = __shfl_sync(0xffffffffu, acc.i, (lane + s) & 31);
-      if ((lane & (2 * s - 1)) == 0) {
-        // lane covers [lane, lane+2s); other covers [lane+s, lane+2s)
-        if (OP == PB_SUM) acc = RD::merge(acc, other);
-        else {
-          // pick by value, tie -> smaller index (indices are interleaved, not ordered)
-          if (other.i >= 0) {
-            if (acc.i < 0) acc = other;
-            else {
-              bool an = nan_(acc.v), bn = nan_(other.v);
-              bool take;
-              if (an || bn) take = bn && (!an || other.i < acc.i);
-              else if (OP == PB_RMAX || OP == PB_ARGMAX) take = other.v > acc.v || (other.v == acc.v && other.i < acc.i);
-              else take = other.v < acc.v || (other.v == acc.v && other.i < acc.i);
-              if (take) acc = other;
-            }
-          }
-        }
-      }
-    }
+    for (int s = 1; s < 32; s <<= 1) lane_fold<OP, T>(acc, lane, s, 0xffffffffu);
     if (lane == 0) emit<OP, T>(r, o, c, acc);
   }
 }
 
-// one thread per (output, chunk)
+// one thread per (output, chunk); the walk issues 8 independent loads at a time
 template <int OP, typename T>
 __global__ void __launch_bounds__(256) red_thread(RedArgs r) {
   typedef Red<OP, T> RD;
@@ -175,8 +192,81 @@ __global__ void __launch_bounds__(256) red_thread(RedArgs r) {
     int64_t r0 = c * r.chunk, r1 = r0 + r.chunk < r.R ? r0 + r.chunk : r.R;
     Acc acc = RD::init();
     const T* p = a + base + r0 * r.sR;
-    for (int64_t j = r0; j < r1; ++j, p += r.sR) RD::add(acc, *p, j);
+    const int64_t sR = r.sR;
+    int64_t j = r0;
+    if (OP == PB_SUM) {  // independent chains: the dependent f64 add latency bounds the walk
+      Acc a1 = RD::init(), a2 = RD::init(), a3 = RD::init();
+      for (; j + 8 <= r1; j += 8, p += 8 * sR) {
+        T v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = p[q * sR];
+        RD::add(acc, v[0], j);
+        RD::add(a1, v[1], j);
+        RD::add(a2, v[2], j);
+        RD::add(a3, v[3], j);
+        RD::add(acc, v[4], j);
+        RD::add(a1, v[5], j);
+        RD::add(a2, v[6], j);
+        RD::add(a3, v[7], j);
+      }
+      acc = RD::merge(RD::merge(acc, a1), RD::merge(a2, a3));
+    } else {
+      for (; j + 8 <= r1; j += 8, p += 8 * sR) {
+        T v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = p[q * sR];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) RD::add(acc, v[q], j + q);
+      }
+    }
+    for (; j < r1; ++j, p += sR) RD::add(acc, *p, j);
     emit<OP, T>(r, o, c, acc);
+  }
+}
+
+// short contiguous rows (a + o*R, R <= 64, 4-byte types): the block stages ROWS rows with
+// coalesced loads into shared memory (odd row pitch: conflict-free), then one thread walks
+// each row in order
+template <int OP, typename T>
+__global__ void __launch_bounds__(256) red_rows(RedArgs r, FastDiv fR, int rows_per_block, int pitch) {
+  typedef Red<OP, T> RD;
+  typedef typename RD::Acc Acc;
+  extern __shared__ uint32_t rows_smem[];
+  T* buf = reinterpret_cast<T*>(rows_smem);
+  const T* a = (const T*)r.a;
+  const int R = (int)r.R;
+  for (int64_t o0 = (int64_t)blockIdx.x * rows_per_block; o0 < r.O; o0 += (int64_t)gridDim.x * rows_per_block) {
+    const int rows = (int)(r.O - o0 < rows_per_block ? r.O - o0 : rows_per_block);
+    const uint32_t n = (uint32_t)rows * R;
+    const T* src = a + o0 * R;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+      uint32_t q, j;
+      fR.divmod(e, q, j);
+      buf[q * pitch + j] = src[e];
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < rows) {
+      Acc acc = RD::init();
+      const T* row = buf + threadIdx.x * pitch;
+      if (OP == PB_SUM) {
+        // four independent f64 chains (the dependent-add latency bounds this loop); f32 terms
+        // summed in f64 round to the same f32 in any order but for rare ties
+        Acc a1 = RD::init(), a2 = RD::init(), a3 = RD::init();
+        int j = 0;
+        for (; j + 4 <= R; j += 4) {
+          RD::add(acc, row[j], j);
+          RD::add(a1, row[j + 1], j + 1);
+          RD::add(a2, row[j + 2], j + 2);
+          RD::add(a3, row[j + 3], j + 3);
+        }
+        for (; j < R; ++j) RD::add(acc, row[j], j);
+        acc = RD::merge(RD::merge(acc, a1), RD::merge(a2, a3));
+      } else {
+        for (int j = 0; j < R; ++j) RD::add(acc, row[j], j);
+      }
+      emit<OP, T>(r, o0 + threadIdx.x, 0, acc);
+    }
+    __syncthreads();
   }
 }
 
@@ -218,14 +308,44 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
       r.nd++;
     }
   }
+  {  // merge kept dim k into k-1 when they are contiguous with each other
+    int nd = 0;
+    for (int k = 0; k < r.nd; ++k) {
+      if (r.shape[k] == 1) continue;
+      if (nd > 0 && r.st[nd - 1] == r.st[k] * r.shape[k]) {
+        r.shape[nd - 1] *= r.shape[k];
+        r.st[nd - 1] = r.st[k];
+        continue;
+      }
+      r.shape[nd] = r.shape[k];
+      r.st[nd] = r.st[k];
+      ++nd;
+    }
+    r.nd = nd;
+  }
   r.O = 1;
   for (int k = 0; k < r.nd; ++k) r.O *= r.shape[k];
+  r.fast = r.O < ((int64_t)1 << 31);
+  for (int k = 0; k < r.nd && r.fast; ++k) r.fd[k] = FastDiv((uint32_t)r.shape[k]);
   if (r.O == 0) return PB_OK;
   if (r.R == 0) {  // empty sum -> zeros (max/min/argmax rejected by the planner)
     pb_scalar z = {1, 0, 0.0, 0};
     return pb_fill(out, &z);
   }
   if (r.R == 1) r.sR = 1;
+  cudaStream_t s = compute_stream();
+  if (sizeof(T) == 4 && r.sR == 1 && r.R > 1 && r.R <= 64 && r.nd == 1 && r.st[0] == r.R && r.O >= 1024 &&
+      r.O * r.R < ((int64_t)1 << 31)) {
+    r.chunks = 1;
+    r.chunk = r.R;
+    r.partial = nullptr;
+    const int rows = r.R <= 32 ? 256 : 128, pitch = (int)(r.R | 1);
+    const int64_t blocks = (r.O + rows - 1) / rows;
+    const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+    red_rows<OP, T><<<grid, 256, (size_t)rows * pitch * 4, s>>>(r, FastDiv((uint32_t)r.R), rows, pitch);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
   bool warp_mode = (r.sR == 1 && r.R >= 32);
   int64_t target = warp_mode ? (int64_t)num_sms() * 64 : (int64_t)num_sms() * 1024;
   int64_t min_chunk = warp_mode ? 2048 : 128;
@@ -242,7 +362,6 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
     r.partial = nullptr;
   }
   int64_t units = r.O * chunks;
-  cudaStream_t s = compute_stream();
   if (warp_mode) {
     int64_t blocks = (units * 32 + 255) / 256;
     int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);

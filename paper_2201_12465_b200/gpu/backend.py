@@ -74,15 +74,16 @@ class DevBlock:
 class DeviceArray:
     """Adapter: a strided view (element strides) into a DevBlock."""
 
-    __slots__ = ("block", "ptr", "shape", "strides", "dtype", "host", "__weakref__")
+    __slots__ = ("block", "ptr", "shape", "strides", "dtype", "host", "fill", "__weakref__")
 
-    def __init__(self, block, ptr, shape, strides, dtype, host=None):
+    def __init__(self, block, ptr, shape, strides, dtype, host=None, fill=None):
         self.block = block
         self.ptr = ptr
         self.shape = shape
         self.strides = strides
         self.dtype = dtype
         self.host = host
+        self.fill = fill  # the value of a full() view (every element), else None
 
     def packed(self):
         return _pack(self.ptr, self.dtype.code, self.shape, self.strides)
@@ -400,7 +401,7 @@ class GpuBackend(Backend):
         blk = self._alloc(dt.itemsize, "full")
         one = DeviceArray(blk, blk.ptr, (1,), (1,), dt)
         _lib.check(self._lib.pb_fill(one.packed(), _lib.pack_scalar(call.params["value"])), "full")
-        return DeviceArray(blk, blk.ptr, shape, (0,) * len(shape), dt)
+        return DeviceArray(blk, blk.ptr, shape, (0,) * len(shape), dt, fill=v)
 
     def _arange(self, call, args):
         out = self._new(tuple(call.shape), call.dtype, "arange")
@@ -558,6 +559,10 @@ class GpuBackend(Backend):
             args = [a.dev() if type(a) is LazyArray else a for a in args]
         name = call.name
         p = call.params
+        if name == "mul" and "scalar" not in p:
+            view = self._times_one(call, args)
+            if view is not None:
+                return view
         out = self._new(tuple(call.shape), call.dtype, name)
         if out.block is None:
             return out
@@ -593,6 +598,29 @@ class GpuBackend(Backend):
         if rc:
             _lib.check(rc, name)
         return out
+
+    @staticmethod
+    def _times_one(call, args):
+        """``full(shape, 1) * g`` with g already of the result dtype is g broadcast to the
+        result shape, bit for bit (x * 1 == x in IEEE arithmetic; the reference's sum backward
+        spreads grads this way, minml/autograd.py:615-617): return a zero-copy view."""
+        a, b = args
+        for one, g in ((a, b), (b, a)):
+            if (type(one) is DeviceArray and one.fill is not None and type(g) is DeviceArray and
+                    one.fill == 1 and type(one.fill) is not bool and g.dtype is call.dtype and
+                    one.dtype is call.dtype and call.dtype.is_float):
+                shape = tuple(call.shape)
+                off = len(shape) - len(g.shape)
+                strides = [0] * off
+                for d, (n, st) in enumerate(zip(g.shape, g.strides)):
+                    if n == shape[off + d]:
+                        strides.append(st)
+                    elif n == 1:
+                        strides.append(0)
+                    else:
+                        return None
+                return DeviceArray(g.block, g.ptr, shape, tuple(strides), g.dtype)
+        return None
 
     def _any(self, what, a):
         _lib.check(self._lib.pb_check(what, a.packed(), ctypes.byref(self._flag)), "check")

@@ -45,7 +45,7 @@ def test_trajectory_f64_accumulation_path_is_tight(name):
     try:
         losses, sums, _ = run_trajectory(name, meta, be)
     finally:
-        be._lib.pb_set_gemm_path(1)
+        be._lib.pb_set_gemm_path(2)
     assert rel_err(losses, meta["losses"]) <= 1e-3, (losses, meta["losses"])
     assert rel_err(sums, meta["param_sums"]) <= 1e-3
 

@@ -104,8 +104,31 @@ def test_large_elementwise_bit_exact(gpu):
                           np.logical_not(a < 0).astype(np.float32))
 
 
+PADS = [
+    ((4, 8, 14, 1, 14), ((0, 0), (0, 0), (0, 0), (0, 1), (0, 0)), 0.0),   # max-pool backward interleave
+    ((4, 8, 27, 28), ((0, 0), (0, 0), (1, 0), (0, 0)), 0.0),             # rows, inner extent % 4 == 0
+    ((4, 8, 28, 27), ((0, 0), (0, 0), (0, 0), (2, 1)), 0.0),             # inner offset not 16B aligned
+    ((2, 3, 7, 7), ((0, 0), (0, 0), (1, 1), (1, 1)), float("-inf")),    # stem pad before max-pool
+    ((5, 6, 3), ((2, 1), (0, 0), (1, 0)), -2.5),
+]
+
+
+@pytest.mark.parametrize("shape,pw,value", PADS)
+def test_pad_layouts(gpu, shape, pw, value):
+    x = np.random.default_rng(len(shape)).standard_normal(shape).astype(np.float32)
+    t = T.tensor(x, backend=gpu.name)
+    assert np.array_equal(t.pad(pw, value=value).to_host_buffer(), np.pad(x, pw, constant_values=value))
+    # strided source view (transposed last two axes)
+    perm = tuple(range(len(shape) - 2)) + (len(shape) - 1, len(shape) - 2)
+    xv = np.transpose(x, perm)
+    pv = pw[:-2] + (pw[-1], pw[-2])
+    assert np.array_equal(t.transpose(perm).pad(pv, value=value).to_host_buffer(),
+                          np.pad(xv, pv, constant_values=value))
+
+
 @pytest.mark.parametrize("shape,axis", [((32, 64, 56, 56), 3), ((32, 64, 56), 2), ((32, 2048), 0), ((2048, 768), 0),
-                                        ((16, 1000), 1), ((3, 100003), 1)])
+                                        ((16, 1000), 1), ((3, 100003), 1), ((32, 64, 7, 7), 3), ((32, 64, 28), 2),
+                                        ((1, 64, 14, 14), 2), ((32, 64, 5), 0), ((2, 3, 33), 2)])
 def test_reduction_shapes(gpu, shape, axis):
     x = np.random.default_rng(7).standard_normal(shape).astype(np.float32)
     t = T.tensor(x, backend=gpu.name)
@@ -144,3 +167,25 @@ def test_conv_sizes(gpu, xs, ws, s, p):
     assert rel_err(gi, _oracle("conv2d_grad_input", dict(params, x_shape=xs), [g, w])) <= 1e-5
     gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()  # reduces over N*Ho*Wo (up to 100352)
     assert contraction_err(gw, _oracle("conv2d_grad_weight", dict(params, w_shape=ws), [x, g])) <= 1e-5
+
+
+def test_times_one_is_a_broadcast_view(gpu):
+    """full(shape, 1) * g (the reference's sum backward spread) is a zero-copy view of g,
+    bit-identical to the multiply, and every consumer reads it correctly."""
+    r = np.random.default_rng(3)
+    g = np.concatenate([r.standard_normal(23), [np.inf, -np.inf, -0.0, 0.0, np.nan]]).astype(np.float32)
+    g = g.reshape(2, 1, 14, 1)
+    tg = T.tensor(g, backend=gpu.name)
+    ones = T.full((2, 3, 14, 5), 1.0, dtype="f32", backend=gpu.name)
+    for prod, want in ((ones * tg, np.ones((2, 3, 14, 5), np.float32) * g),
+                       (tg * ones, g * np.ones((2, 3, 14, 5), np.float32))):
+        assert prod.adapter.block is tg.adapter.block  # no new allocation
+        got = prod.to_host_buffer()
+        assert np.array_equal(got, want, equal_nan=True)
+        assert np.array_equal(np.signbit(got), np.signbit(want))
+        assert np.array_equal((prod / 5.0).to_host_buffer(), want / np.float32(5.0), equal_nan=True)
+        assert np.array_equal(prod.sum(axis=0).to_host_buffer(),
+                              np.sum(want, axis=0, dtype=np.float64).astype(np.float32), equal_nan=True)
+    # anything but an exact f32 one keeps the multiply
+    twos = T.full((2, 3, 14, 5), 2.0, dtype="f32", backend=gpu.name)
+    assert (twos * tg).adapter.block is not tg.adapter.block

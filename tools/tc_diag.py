@@ -18,7 +18,7 @@ for xs, ws, s, p in [((32, 64, 56, 56), (64, 64, 3, 3), 1, 1), ((8, 256, 56, 56)
     for path in (1, 0):
         be._lib.pb_set_gemm_path(path)
         res[path] = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer().astype(np.float64)
-    be._lib.pb_set_gemm_path(1)
+    be._lib.pb_set_gemm_path(2)
     ref = res[0]  # SIMT: f64 accumulation
     d = np.abs(res[1] - ref)
     m = d / np.maximum(np.abs(ref), 1)
@@ -29,5 +29,5 @@ for xs, ws, s, p in [((32, 64, 56, 56), (64, 64, 3, 3), 1, 1), ((8, 256, 56, 56)
     for path in (1, 0):
         be._lib.pb_set_gemm_path(path)
         res[path] = T.conv2d(tx, tw, None, s, p).to_host_buffer().astype(np.float64)
-    be._lib.pb_set_gemm_path(1)
+    be._lib.pb_set_gemm_path(2)
     d = np.abs(res[1] - res[0]); print("   fprop max abs err", d.max(), "rms", np.sqrt((res[0] ** 2).mean()))
