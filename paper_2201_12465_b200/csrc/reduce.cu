@@ -224,47 +224,59 @@ __global__ void __launch_bounds__(256) red_thread(RedArgs r) {
   }
 }
 
-// short contiguous rows (a + o*R, R <= 64, 4-byte types): the block stages ROWS rows with
-// coalesced loads into shared memory (odd row pitch: conflict-free), then one thread walks
-// each row in order
+// short contiguous rows (a + o*R, R <= 128, 4-byte types): the block copies ROWS whole rows
+// -- one contiguous span -- into shared memory with coalesced (16-byte when aligned) loads, then
+// thread t < ROWS walks row t.  Sums of even-length rows walk the row rotated by t (element
+// (j + t) mod R), which makes the strided shared-memory reads bank-conflict free; f32 terms summed in f64
+// give the same f32 result in any order (but for rare ties).  Extrema walk in index order.
 template <int OP, typename T>
-__global__ void __launch_bounds__(256) red_rows(RedArgs r, FastDiv fR, int rows_per_block, int pitch) {
+__global__ void __launch_bounds__(256) red_rows(RedArgs r, int rows_per_block, int vec) {
   typedef Red<OP, T> RD;
   typedef typename RD::Acc Acc;
-  extern __shared__ uint32_t rows_smem[];
-  T* buf = reinterpret_cast<T*>(rows_smem);
+  extern __shared__ float4 rows_smem4[];
+  T* buf = reinterpret_cast<T*>(rows_smem4);
   const T* a = (const T*)r.a;
   const int R = (int)r.R;
   for (int64_t o0 = (int64_t)blockIdx.x * rows_per_block; o0 < r.O; o0 += (int64_t)gridDim.x * rows_per_block) {
     const int rows = (int)(r.O - o0 < rows_per_block ? r.O - o0 : rows_per_block);
-    const uint32_t n = (uint32_t)rows * R;
+    const int n = rows * R;
     const T* src = a + o0 * R;
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
-      uint32_t q, j;
-      fR.divmod(e, q, j);
-      buf[q * pitch + j] = src[e];
+    int e0 = 0;
+    if (vec) {  // o0 * R % 4 == 0 and the base is 16-byte aligned
+      const int n4 = n >> 2;
+      const float4* s4 = reinterpret_cast<const float4*>(src);
+      for (int q = threadIdx.x; q < n4; q += blockDim.x) rows_smem4[q] = __ldg(s4 + q);
+      e0 = n4 << 2;
     }
+    for (int e = e0 + threadIdx.x; e < n; e += blockDim.x) buf[e] = src[e];
     __syncthreads();
     if ((int)threadIdx.x < rows) {
+      const int t = threadIdx.x;
+      const T* row = buf + t * R;
       Acc acc = RD::init();
-      const T* row = buf + threadIdx.x * pitch;
       if (OP == PB_SUM) {
-        // four independent f64 chains (the dependent-add latency bounds this loop); f32 terms
-        // summed in f64 round to the same f32 in any order but for rare ties
         Acc a1 = RD::init(), a2 = RD::init(), a3 = RD::init();
-        int j = 0;
-        for (; j + 4 <= R; j += 4) {
+        int j = (R & 1) ? 0 : t % R;  // rotate even rows (odd R is conflict free as is)
+        int k = 0;
+        for (; k + 4 <= R; k += 4) {
           RD::add(acc, row[j], j);
-          RD::add(a1, row[j + 1], j + 1);
-          RD::add(a2, row[j + 2], j + 2);
-          RD::add(a3, row[j + 3], j + 3);
+          j = j + 1 == R ? 0 : j + 1;
+          RD::add(a1, row[j], j);
+          j = j + 1 == R ? 0 : j + 1;
+          RD::add(a2, row[j], j);
+          j = j + 1 == R ? 0 : j + 1;
+          RD::add(a3, row[j], j);
+          j = j + 1 == R ? 0 : j + 1;
         }
-        for (; j < R; ++j) RD::add(acc, row[j], j);
+        for (; k < R; ++k) {
+          RD::add(acc, row[j], j);
+          j = j + 1 == R ? 0 : j + 1;
+        }
         acc = RD::merge(RD::merge(acc, a1), RD::merge(a2, a3));
       } else {
         for (int j = 0; j < R; ++j) RD::add(acc, row[j], j);
       }
-      emit<OP, T>(r, o0 + threadIdx.x, 0, acc);
+      emit<OP, T>(r, o0 + t, 0, acc);
     }
     __syncthreads();
   }
@@ -334,15 +346,24 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
   }
   if (r.R == 1) r.sR = 1;
   cudaStream_t s = compute_stream();
-  if (sizeof(T) == 4 && r.sR == 1 && r.R > 1 && r.R <= 64 && r.nd == 1 && r.st[0] == r.R && r.O >= 1024 &&
+  if (sizeof(T) == 4 && r.sR == 1 && r.R > 1 && r.R <= 128 && r.nd == 1 && r.st[0] == r.R && r.O >= 1024 &&
       r.O * r.R < ((int64_t)1 << 31)) {
     r.chunks = 1;
     r.chunk = r.R;
     r.partial = nullptr;
-    const int rows = r.R <= 32 ? 256 : 128, pitch = (int)(r.R | 1);
+    const int rows = r.R <= 32 ? 256 : 128;
+    const size_t smem = (size_t)rows * r.R * 4;
+    static bool attr = false;
+    if (!attr) {
+      PB_CUDA(cudaFuncSetAttribute(red_rows<OP, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      attr = true;
+    }
+    const int per_sm = (int)((200 * 1024) / smem) < 8 ? (int)((200 * 1024) / smem) : 8;
     const int64_t blocks = (r.O + rows - 1) / rows;
-    const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
-    red_rows<OP, T><<<grid, 256, (size_t)rows * pitch * 4, s>>>(r, FastDiv((uint32_t)r.R), rows, pitch);
+    const int64_t cap = (int64_t)num_sms() * (per_sm > 0 ? per_sm : 1);
+    const int grid = (int)(blocks < cap ? blocks : cap);
+    const int vec = (rows * r.R) % 4 == 0 && ((uintptr_t)r.a) % 16 == 0;
+    red_rows<OP, T><<<grid, 256, smem, s>>>(r, rows, vec);
     PB_LAUNCHED();
     return PB_OK;
   }
