@@ -237,7 +237,7 @@ def main():
     eager_launches = (be.launch_count() - l0) // n_eager
 
     # ---- whole-step CUDA graph (training.CapturedStep): device-resident replays (value)
-    step = training.CapturedStep(model, opt, ddp=ddp, warmup=1)
+    step = training.CapturedStep(model, opt, ddp=ddp, warmup=2)
     graph_error = None
     try:
         for _ in range(1 + max(args.warmup, 3)):
@@ -297,7 +297,8 @@ def main():
             "config": cfg, "e2e": e2e, "gpu_launches": launches * args.steps, "launches_per_step": launches,
             "roofline": roofline, "clocks": clk.summary(), "final_loss": final_loss,
             "gemm_path": {2: "tcgen05+tma", 1: "tcgen05", 0: "simt"}[be._lib.pb_gemm_path()],
-            "step_mode": "cuda_graph" if step is not None else "eager", "eager": eager}
+            "step_mode": "cuda_graph" if step is not None else "eager", "eager": eager,
+            "fused_ops": step.fused_ops if step is not None else 0}
     if graph_error:
         line["graph_error"] = graph_error
     if world == 1 and not args.no_cpu_baseline:

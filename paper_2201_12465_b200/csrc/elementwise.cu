@@ -354,7 +354,8 @@ struct ChainStep {
 struct ChainArgs {
   const void* leaf[kChainLeaves];
   int8_t is_bool[kChainLeaves];
-  int8_t vec[kChainLeaves];  // chain4: inner stride 1 (else 0)
+  int8_t vec[kChainLeaves];    // chain4: inner stride 1 (else 0)
+  int8_t dense[kChainLeaves];  // chain4x: same strides as the (dense) output: offset = index
   int nleaves, nsteps, head_kind;  // head_kind 0: leaf 0, 1: scalar
   float head_scalar;
   ChainStep step[kChainSteps];
@@ -548,9 +549,73 @@ __global__ void __launch_bounds__(256) ew_chain1(ChainArgs p) {
   }
 }
 
+// 4 consecutive outputs per thread-iteration when rows are not a multiple of 4 (7x7 maps):
+// dense leaves load 16 bytes at the output index, the others decode each element's offset
+__device__ __forceinline__ float4 chain_load4x(const ChainArgs& p, int l, uint32_t e0) {
+  if (p.dense[l]) {
+    if (p.is_bool[l]) {
+      uchar4 u = *reinterpret_cast<const uchar4*>((const uint8_t*)p.leaf[l] + e0);
+      return make_float4(u.x ? 1.f : 0.f, u.y ? 1.f : 0.f, u.z ? 1.f : 0.f, u.w ? 1.f : 0.f);
+    }
+    return __ldg(reinterpret_cast<const float4*>((const float*)p.leaf[l] + e0));
+  }
+  float v[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    uint32_t e = e0 + u;
+    int64_t off = 0;
+#pragma unroll
+    for (int k = 3; k >= 0; --k) {
+      if (k < p.nd) {
+        uint32_t q, r;
+        if (k > 0) {
+          p.ext[k].divmod(e, q, r);
+        } else {
+          q = 0;
+          r = e;
+        }
+        off += (int64_t)r * p.st[l][k];
+        e = q;
+      }
+    }
+    v[u] = chain_load1(p, l, off);
+  }
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
 template <int NL>
-static void launch_chain(ChainArgs& p, bool v4, cudaStream_t s) {
-  if (v4) ew_chain4<NL><<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
+__global__ void __launch_bounds__(256) ew_chain4x(ChainArgs p) {
+  const uint32_t step = gridDim.x * blockDim.x;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t v4 = blockIdx.x * blockDim.x + threadIdx.x; v4 < p.n; v4 += step) {
+    const uint32_t e0 = v4 * 4u;
+    float4 x0 = chain_load4x(p, 0, e0);
+    float4 x1 = NL > 1 ? chain_load4x(p, 1, e0) : z;
+    float4 x2 = NL > 2 ? chain_load4x(p, 2, e0) : z;
+    float4 x3 = NL > 3 ? chain_load4x(p, 3, e0) : z;
+    float4 x4 = NL > 4 ? chain_load4x(p, 4, e0) : z;
+    float4 x5 = NL > 5 ? chain_load4x(p, 5, e0) : z;
+    float4 x6 = NL > 6 ? chain_load4x(p, 6, e0) : z;
+    float4 x7 = NL > 7 ? chain_load4x(p, 7, e0) : z;
+    float4 v = p.head_kind == 0 ? x0 : make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
+    for (int s = 0; s < p.nsteps; ++s) {
+      const ChainStep st = p.step[s];
+      float4 o = v;
+      if (st.kind == 1) o = pick<NL>(st.leaf, x0, x1, x2, x3, x4, x5, x6, x7);
+      else if (st.kind == 2) o = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
+      v = chain_step4(st, v, o);
+    }
+    if (p.out_bool)
+      reinterpret_cast<uchar4*>(p.out)[v4] = make_uchar4(v.x != 0.f, v.y != 0.f, v.z != 0.f, v.w != 0.f);
+    else
+      reinterpret_cast<float4*>(p.out)[v4] = v;
+  }
+}
+
+template <int NL>
+static void launch_chain(ChainArgs& p, int mode, cudaStream_t s) {
+  if (mode == 1) ew_chain4<NL><<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
+  else if (mode == 2) ew_chain4x<NL><<<grid_for(p.n, 256, 2), 256, 0, s>>>(p);
   else ew_chain1<NL><<<grid_for(p.n, 256, 4), 256, 0, s>>>(p);
 }
 
@@ -1097,21 +1162,31 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
     }
   }
   cudaStream_t s = compute_stream();
-  if (v4) {
+  int mode = v4 ? 1 : 0;
+  if (!v4 && n % 4 == 0 && (out->ptr & 15) == 0) {  // chain4x: dense leaves aligned
+    mode = 2;
+    for (int l = 0; l < nleaves; ++l) {
+      bool dense = true;
+      for (int k = 0; k < nd; ++k) dense = dense && cst[l][k] == cst[kChainLeaves][k];
+      p.dense[l] = dense;
+      if (dense && leaves[l].ptr % (p.is_bool[l] ? 4 : 16)) mode = 0;
+    }
+  }
+  if (mode == 1) {
     p.n = (uint32_t)(n / 4);
   } else {
     for (int l = 0; l < kChainLeaves; ++l) p.vec[l] = 0;
-    p.n = (uint32_t)n;
+    p.n = (uint32_t)(mode == 2 ? n / 4 : n);
   }
   switch (nleaves) {
-    case 0: case 1: launch_chain<1>(p, v4, s); break;
-    case 2: launch_chain<2>(p, v4, s); break;
-    case 3: launch_chain<3>(p, v4, s); break;
-    case 4: launch_chain<4>(p, v4, s); break;
-    case 5: launch_chain<5>(p, v4, s); break;
-    case 6: launch_chain<6>(p, v4, s); break;
-    case 7: launch_chain<7>(p, v4, s); break;
-    default: launch_chain<8>(p, v4, s); break;
+    case 0: case 1: launch_chain<1>(p, mode, s); break;
+    case 2: launch_chain<2>(p, mode, s); break;
+    case 3: launch_chain<3>(p, mode, s); break;
+    case 4: launch_chain<4>(p, mode, s); break;
+    case 5: launch_chain<5>(p, mode, s); break;
+    case 6: launch_chain<6>(p, mode, s); break;
+    case 7: launch_chain<7>(p, mode, s); break;
+    default: launch_chain<8>(p, mode, s); break;
   }
   PB_LAUNCHED();
   return PB_OK;

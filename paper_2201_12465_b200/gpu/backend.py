@@ -16,6 +16,7 @@ backend cannot be constructed.
 """
 
 import ctypes
+import weakref
 import os
 import sys
 
@@ -210,6 +211,15 @@ class GpuBackend(Backend):
         # bit-identical (tests/test_gpu_fusion.py) but the interpreted chain kernel is still
         # ALU-bound -- ResNet-50 measured 576 samples/s fused vs 634 unfused
         self._fuse = (os.environ.get("PB_FUSE", "0") == "1") if fuse is None else bool(fuse)
+        # trace-planned fusion (fusion_trace_* / fusion_plan_*): a traced step tells which
+        # elementwise results have exactly one consumer, itself elementwise; the planned
+        # (captured) step keeps only those lazy, so no chain is ever computed twice
+        self._trace = None
+        self._plan = None
+        self._planned = False
+        self._prod = {}
+        self._op_idx = 0
+        self._lazy_ok = True
         self._lib = _lib.load()
         _lib.check(self._lib.pb_init(device), "pb_init")
         self.device = device
@@ -294,6 +304,11 @@ class GpuBackend(Backend):
 
     # ----------------------------------------------------------------- execute
     def execute(self, call, args):
+        if self._trace is not None or self._planned:
+            return self._execute_traced(call, args)
+        return self._execute(call, args)
+
+    def _execute(self, call, args):
         name = call.name
         if name not in _FUSE_BIN and name not in _FUSE_UN:
             args = [a.dev() if type(a) is LazyArray else a for a in args]
@@ -305,6 +320,69 @@ class GpuBackend(Backend):
             finally:
                 ledger.on_op_end(call.name)
         return self._ops[call.name](call, args)
+
+    # ------------------------------------------------------- planned fusion
+    def _producer(self, a):
+        e = self._prod.get(id(a))
+        return e[0] if e is not None and e[1]() is a else -1
+
+    def _execute_traced(self, call, args):
+        idx = self._op_idx
+        self._op_idx += 1
+        name = call.name
+        fusible = name in _FUSE_BIN or name in _FUSE_UN
+        sig = (name, tuple(call.shape), call.dtype.name, tuple(tuple(a.shape) for a in args))
+        prods = tuple(self._producer(a) for a in args)
+        if self._trace is not None:
+            self._trace.append((sig, prods, fusible))
+        else:
+            tr, lazy = self._plan
+            if idx < len(tr) and tr[idx][0] == sig and tr[idx][1] == prods:
+                self._lazy_ok = lazy[idx]
+            else:  # the step diverged from the trace: stop fusing (everything materialises)
+                self._abandon_plan()
+        res = self._execute(call, args)
+        if type(res) is DeviceArray or type(res) is LazyArray:
+            self._prod[id(res)] = (idx, weakref.ref(res))
+        return res
+
+    def fusion_trace_begin(self):
+        """Record the op stream of one (eager) step: signatures and producer links."""
+        self._trace, self._prod, self._op_idx = [], {}, 0
+
+    def fusion_trace_end(self):
+        """Build the plan: an elementwise f32/bool result may stay lazy iff the traced step
+        consumed it exactly once, by an elementwise op.  Returns the number of such ops."""
+        tr, self._trace, self._prod = self._trace, None, {}
+        n = len(tr)
+        uses, by_fusible = [0] * n, [True] * n
+        for sig, prods, fusible in tr:
+            for q in prods:
+                if q >= 0:
+                    uses[q] += 1
+                    by_fusible[q] = by_fusible[q] and fusible
+        lazy = [tr[i][2] and uses[i] == 1 and by_fusible[i] for i in range(n)]
+        self._plan = (tr, lazy)
+        return sum(lazy)
+
+    def fusion_plan_begin(self):
+        """Replay the planned step (normally while recording a CUDA graph): ops the plan marks
+        stay lazy and fold into their single consumer's chain kernel."""
+        if self._plan is None:
+            return False
+        self._planned, self._prod, self._op_idx = True, {}, 0
+        self._fuse_saved, self._fuse = self._fuse, True
+        return True
+
+    def _abandon_plan(self):
+        self._lazy_ok = False
+        self._plan = ([], [])
+
+    def fusion_plan_end(self):
+        if self._planned:
+            self._planned, self._prod = False, {}
+            self._fuse = self._fuse_saved
+        self._lazy_ok = True
 
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
@@ -552,17 +630,18 @@ class GpuBackend(Backend):
 
     # elementwise
     def _binary(self, call, args):
-        if self._fuse:
-            lz = self._try_fuse_binary(call, args)
-            if lz is not None:
-                return lz
-            args = [a.dev() if type(a) is LazyArray else a for a in args]
         name = call.name
         p = call.params
         if name == "mul" and "scalar" not in p:
             view = self._times_one(call, args)
             if view is not None:
                 return view
+        if self._fuse and (self._lazy_ok or type(args[0]) is LazyArray or
+                           (len(args) > 1 and type(args[1]) is LazyArray)):
+            lz = self._try_fuse_binary(call, args)
+            if lz is not None:
+                return lz if self._lazy_ok else lz.dev()
+            args = [a.dev() if type(a) is LazyArray else a for a in args]
         out = self._new(tuple(call.shape), call.dtype, name)
         if out.block is None:
             return out
@@ -631,10 +710,10 @@ class GpuBackend(Backend):
             raise DomainError(msg)
 
     def _unary(self, call, args):
-        if self._fuse:
+        if self._fuse and (self._lazy_ok or type(args[0]) is LazyArray):
             lz = self._try_fuse_unary(call, args)
             if lz is not None:
-                return lz
+                return lz if self._lazy_ok else lz.dev()
             args = [a.dev() if type(a) is LazyArray else a for a in args]
         a = args[0]
         out = self._new(tuple(call.shape), call.dtype, call.name)

@@ -66,7 +66,10 @@ class CapturedStep:
     forward, cross-entropy, backward, [bucketed allreduce], SGD -- into a CUDA graph, and
     every later call is: copy the batch into the graph's static input buffers, launch the
     graph, read the loss.  Results are those of ``train_step``: the same kernels run in
-    the same order on the same buffers.
+    the same order on the same buffers -- except that, with ``fuse`` (the default), the last
+    warm-up step is traced and the recorded step runs every elementwise result whose only
+    consumer is elementwise inside that consumer's chain kernel (GpuBackend.fusion_*; the
+    chain kernel is bit-identical to the unfused primitives).
 
     State the step rebinds instead of updating in place (e.g. BatchNorm running stats,
     minml/nn.py:299-300) is copied back into its original buffer at the end of the graph,
@@ -74,10 +77,14 @@ class CapturedStep:
     be recorded: their counter offset is reserved on the host per call.
     """
 
-    def __init__(self, model, optimizer, ddp=None, warmup=1):
+    def __init__(self, model, optimizer, ddp=None, warmup=2, fuse=True):
         self.model, self.opt, self.ddp = model, optimizer, ddp
         self.backend = registry.get(model_backend(model))
         self.warmup = int(warmup)
+        # trace-planned elementwise fusion: the last warm-up step is traced, the recorded
+        # step fuses every elementwise result whose single consumer is elementwise
+        self.fuse = bool(fuse) and self.warmup >= 2 and hasattr(self.backend, "fusion_trace_begin")
+        self.fused_ops = 0
         self.calls = 0
         self.graph = None
         self.x = self.y = None
@@ -136,7 +143,14 @@ class CapturedStep:
             be.copy_in(self.y, labels)
         self.calls += 1
         if self.graph is None and self.calls <= self.warmup:
-            loss, out = self._body()
+            trace = self.fuse and self.calls == self.warmup
+            if trace:
+                be.fusion_trace_begin()
+            try:
+                loss, out = self._body()
+            finally:
+                if trace:
+                    self.fused_ops = be.fusion_trace_end()
             return loss.scalar(), out
         if self.graph is None:
             self._capture()
@@ -147,9 +161,14 @@ class CapturedStep:
         be = self.backend
         slots = [(o, k, self._get(o, k)) for o, k, _ in self._slots()]
         n0 = be.launch_count()
+        planned = self.fuse and be.fusion_plan_begin()
         be.capture_begin()
         try:
-            loss, out = self._body()
+            try:
+                loss, out = self._body()
+            finally:
+                if planned:
+                    be.fusion_plan_end()
         except BaseException:
             try:
                 be.capture_end()  # discard the partial recording

@@ -12,14 +12,14 @@ from paper_2201_12465_b200 import errors, models, optim, training
 pytestmark = pytest.mark.gpu
 
 
-def _run(name, be, captured, steps, batch, shape, classes, seed=3):
+def _run(name, be, captured, steps, batch, shape, classes, seed=3, fuse=False):
     be.seed(seed)
     model = BUILDERS[name](be.name)
     opt = optim.SGD(model.params(), lr=0.05, momentum=0.9)
     r = np.random.default_rng(0)
     data = [(r.standard_normal((batch,) + shape).astype(np.float32), r.integers(0, classes, batch).astype(np.int64))
             for _ in range(2)]
-    step = training.CapturedStep(model, opt, warmup=1) if captured else None
+    step = (training.CapturedStep(model, opt, warmup=2 if fuse else 1, fuse=fuse) if captured else None)
     losses = []
     for k in range(steps):
         x, y = data[k % 2]
@@ -50,6 +50,22 @@ def test_captured_step_bit_identical_to_eager(name, shape, classes):
     assert step.graph is not None and step.launches > 20
     assert eager[0] == graph[0], (eager[0], graph[0])
     for a, b in zip(eager[1] + eager[2] + eager[3], graph[1] + graph[2] + graph[3]):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("name,shape,classes", [("lenet", (1, 28, 28), 10), ("resnet_tiny", (3, 32, 32), 10)])
+def test_planned_fusion_bit_identical_and_fewer_launches(name, shape, classes):
+    """The traced-then-planned fusion (GpuBackend.fusion_*) folds single-consumer elementwise
+    results into chain kernels: fewer launches, bit-identical losses and state."""
+    be = gpu_backend()
+    eager = _run(name, be, False, 6, 4, shape, classes)
+    plain = _run(name, be, True, 6, 4, shape, classes)
+    fused = _run(name, be, True, 6, 4, shape, classes, fuse=True)
+    step = fused[4]
+    assert step.fused_ops > 0 and step.launches < plain[4].launches, (step.fused_ops, step.launches,
+                                                                     plain[4].launches)
+    assert eager[0] == fused[0], (eager[0], fused[0])
+    for a, b in zip(eager[1] + eager[2] + eager[3], fused[1] + fused[2] + fused[3]):
         assert np.array_equal(a, b)
 
 
