@@ -288,9 +288,16 @@ def main():
     hbm, tc, src = peaks()
     rl = kernel_roofline(be, T, hbm, tc)
     dom = rl["conv"]
+    # traffic: dram read + write of the TMA conv kernel for this shape in one ncu --set full
+    # capture (profiles/r1/ncu_tma_conv_56x56.txt: 51.73 MB read + 1.60 MB written per launch;
+    # the hi/lo operand planes are read once, the output stays in L2 during the kernel)
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                "frac": dom["achieved"] / dom["peak"], "traffic": None, "kernel": dom["kernel"],
-                "peak_source": src, "other": {k: {kk: v for kk, v in d.items()} for k, d in rl.items() if k != "conv"}}
+                "frac": dom["achieved"] / dom["peak"], "traffic": 53.33e6, "traffic_unit": "bytes/launch",
+                "kernel": dom["kernel"], "peak_source": src,
+                "note": "achieved = useful FLOPs (2*N*F*Ho*Wo*C*kh*kw) / op time incl. the hi/lo pre-pass; "
+                        "3xTF32 issues 3 tf32 MMAs per useful MAC, so the useful ceiling is tf32 peak / 3",
+                "frac_of_3xtf32_ceiling": dom["achieved"] / (tc / 2 / 3),
+                "other": {k: {kk: v for kk, v in d.items()} for k, d in rl.items() if k != "conv"}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) images)",

@@ -486,7 +486,9 @@ __global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi
     float h, l;
     split_hl(w[idx], h, l);
     int64_t d;
-    if (!dgrad) {
+    if (dgrad == 2) {  // columns of the strided dgrad GEMM: [(c, r, s)][f]
+      d = ((int64_t)c * RS + rs) * F + f;
+    } else if (!dgrad) {
       d = ((int64_t)f * RS + rs) * Cc + c;
     } else {
       const int r = rs / KW, s = rs - r * KW;
@@ -495,6 +497,38 @@ __global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi
     }
     hi[d] = h;
     lo[d] = l;
+  }
+}
+
+// strided dgrad, second half: dx[n][c][h][w] = sum over the taps (r, s) that land on the
+// stride grid of Y[(c, r, s)][(n, ho, wo)], ho = (h + ph - r) / sh; taps in (r, s) order, f64
+__global__ void __launch_bounds__(256) col2im_dgrad(const float* __restrict__ Y, float* __restrict__ dx, int N, int C,
+                                                    int H, int W, int KH, int KW, int SH, int SW, int PH, int PW,
+                                                    int HO, int WO) {
+  const int64_t total = (int64_t)N * C * H * W;
+  const int64_t P = (int64_t)N * HO * WO;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int w = (int)(i % W);
+    int64_t t = i / W;
+    const int h = (int)(t % H);
+    t /= H;
+    const int c = (int)(t % C);
+    const int n = (int)(t / C);
+    double acc = 0.0;
+    for (int r = 0; r < KH; ++r) {
+      const int hh = h + PH - r;
+      if (hh < 0 || hh % SH) continue;
+      const int ho = hh / SH;
+      if (ho >= HO) continue;
+      for (int s = 0; s < KW; ++s) {
+        const int ww = w + PW - s;
+        if (ww < 0 || ww % SW) continue;
+        const int wo = ww / SW;
+        if (wo >= WO) continue;
+        acc += (double)__ldg(Y + ((int64_t)(c * KH + r) * KW + s) * P + ((int64_t)n * HO + ho) * WO + wo);
+      }
+    }
+    dx[i] = (float)acc;
   }
 }
 
@@ -584,6 +618,9 @@ int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias,
   const int F = (int)w->shape[0], KH = (int)w->shape[2], KW = (int)w->shape[3];
   Prob pr = make_prob(N, H, W, C, KH, KW, p->stride_h, p->stride_w, p->pad_h, p->pad_w);
   if (!geometry_ok(pr) || F == 0 || N == 0) return PB_ERR_UNSUPPORTED;
+  // 1x1 convs over large planes are bound by the hi/lo pre-pass (measured: 56x56 at b32
+  // runs faster on gemm_tc.cu, which reads x once); 3x3 and the smaller planes win here
+  if (KH * KW == 1 && (int64_t)N * H * W > 25088) return PB_ERR_UNSUPPORTED;
   const int64_t act = (int64_t)N * C * H * W, K = (int64_t)C * KH * KW, rows = (int64_t)N * pr.HO * pr.WO;
   if (!fits(act) || !fits(rows * F) || !fits(K * F) || F % 4 != 0) return PB_ERR_UNSUPPORTED;
   pr.F = F;
@@ -636,12 +673,46 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
                  p->stride_h, p->stride_w, W, H * W};
     return run_conv(pr, gh, gl, wh, wl, o);
   }
-  if (p->stride_h != 1 || p->stride_w != 1) return PB_ERR_UNSUPPORTED;
+  if ((p->stride_h != 1 || p->stride_w != 1) && (int64_t)N * HO * WO <= 8192) {
+    // strided k x k: Y = W^T g as a GEMM over the gradient pixels (rows) and the (c, r, s)
+    // columns, then col2im gathers each dx pixel's on-grid taps.  Measured: wins up to
+    // N*HO*WO = 6272 (b32 at 14x14); at 28x28 the 9x-wide Y round trip loses to gemm_tc.cu.
+    Prob pr = make_prob(N, HO, WO, F, 1, 1, 1, 1, 0, 0);
+    const int RS = KH * KW;
+    const int64_t act = (int64_t)N * F * HO * WO, rows = (int64_t)N * HO * WO, cols = (int64_t)Cx * RS;
+    if (!geometry_ok(pr) || Cx == 0 || N == 0 || !fits(act) || !fits(rows * cols) || !fits((int64_t)N * Cx * H * W) ||
+        !fits(cols * F) || ((int64_t)H + 2 * p->pad_h - KH) / p->stride_h + 1 != HO ||
+        ((int64_t)W + 2 * p->pad_w - KW) / p->stride_w + 1 != WO)
+      return PB_ERR_UNSUPPORTED;
+    pr.F = (int)cols;
+    pr.Mi = (int)rows;
+    pr.Nj = (int)cols;
+    pr.K = F;
+    const size_t wb = ((size_t)cols * F * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
+    const size_t yb = (size_t)rows * cols * 4;
+    char* ws = (char*)workspace(2 * wb + 2 * ab + yb);
+    if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
+    float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
+    float* Y = (float*)(ws + 2 * wb + 2 * ab);
+    weight_split<<<grid_for(cols * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx,
+                                                                        KH, KW, 2);
+    PB_LAUNCHED();
+    int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
+    if (rc) return rc;
+    OutMat o{Y, (int)rows, (int)cols, rows, 0};  // Y[(c, r, s)][(n, ho, wo)]
+    rc = run_conv(pr, gh, gl, wh, wl, o);
+    if (rc) return rc;
+    col2im_dgrad<<<grid_for((int64_t)N * Cx * H * W, 256), 256, 0, compute_stream()>>>(
+        Y, (float*)(uintptr_t)out->ptr, N, Cx, H, W, KH, KW, p->stride_h, p->stride_w, p->pad_h, p->pad_w, HO, WO);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
   const int ph = KH - 1 - p->pad_h, pw = KW - 1 - p->pad_w;
   if (ph < 0 || pw < 0) return PB_ERR_UNSUPPORTED;
   // the "conv" runs over g [N, F, HO, WO] and produces [N, Cx, H, W]
   Prob pr = make_prob(N, HO, WO, F, KH, KW, 1, 1, ph, pw);
   if (!geometry_ok(pr) || pr.HO != H || pr.WO != W || Cx == 0 || N == 0 || Cx % 4 != 0) return PB_ERR_UNSUPPORTED;
+  if (KH * KW == 1 && (int64_t)N * H * W > 25088) return PB_ERR_UNSUPPORTED;  // as in fprop
   const int64_t act = (int64_t)N * F * HO * WO, K = (int64_t)F * KH * KW, rows = (int64_t)N * H * W;
   if (!fits(act) || !fits(rows * Cx) || !fits(K * Cx)) return PB_ERR_UNSUPPORTED;
   pr.F = Cx;

@@ -282,6 +282,39 @@ __global__ void __launch_bounds__(256) red_rows(RedArgs r, int rows_per_block, i
   }
 }
 
+// strided reduced axis (sR > 1), R <= 4096: a block owns 32 consecutive outputs (one per lane,
+// so each load instruction is coalesced along the kept inner axis) and splits the reduced axis
+// into 8 contiguous slices (one per warp); the slices fold in order through shared memory.
+// One launch, deterministic, and each thread walks at most R/8 elements.
+template <int OP, typename T>
+__global__ void __launch_bounds__(256) red_cols(RedArgs r) {
+  typedef Red<OP, T> RD;
+  typedef typename RD::Acc Acc;
+  __shared__ Acc part[8][32];
+  const T* a = (const T*)r.a;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t slice = (r.R + 7) / 8;
+  const int64_t j0 = ty * slice, j1 = j0 + slice < r.R ? j0 + slice : r.R;
+  for (int64_t o0 = (int64_t)blockIdx.x * 32; o0 < r.O; o0 += (int64_t)gridDim.x * 32) {
+    const int64_t o = o0 + tx;
+    Acc acc = RD::init();
+    if (o < r.O) {
+      const T* p = a + out_base(r, o);
+      const int64_t sR = r.sR;
+#pragma unroll 4
+      for (int64_t j = j0; j < j1; ++j) RD::add(acc, p[j * sR], j);
+    }
+    part[ty][tx] = acc;
+    __syncthreads();
+    if (ty == 0 && o < r.O) {
+#pragma unroll
+      for (int t = 1; t < 8; ++t) acc = RD::merge(acc, part[t][tx]);
+      emit<OP, T>(r, o, 0, acc);
+    }
+    __syncthreads();
+  }
+}
+
 // fold chunk partials in chunk order
 template <int OP, typename T>
 __global__ void __launch_bounds__(256) red_final(RedArgs r) {
@@ -364,6 +397,16 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
     const int grid = (int)(blocks < cap ? blocks : cap);
     const int vec = (rows * r.R) % 4 == 0 && ((uintptr_t)r.a) % 16 == 0;
     red_rows<OP, T><<<grid, 256, smem, s>>>(r, rows, vec);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
+  if (r.sR > 1 && r.R <= 4096) {
+    r.chunks = 1;
+    r.chunk = r.R;
+    r.partial = nullptr;
+    const int64_t blocks = (r.O + 31) / 32;
+    const int grid = (int)(blocks < (int64_t)num_sms() * 16 ? blocks : (int64_t)num_sms() * 16);
+    red_cols<OP, T><<<grid, 256, 0, s>>>(r);
     PB_LAUNCHED();
     return PB_OK;
   }
