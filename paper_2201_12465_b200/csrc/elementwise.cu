@@ -1041,28 +1041,43 @@ __global__ void __launch_bounds__(256) pad_fast(PadFast p, uint32_t value) {
 
 // innermost output extent % 4 == 0: one index decomposition per 4 consecutive outputs of a
 // row, 16-byte stores
+__device__ __forceinline__ void pad_row(const PadFast& p, uint32_t row, int64_t& so, bool& inside) {
+  so = 0;
+  inside = true;
+  for (int k = p.nd - 2; k >= 0; --k) {
+    uint32_t q2, r;
+    p.ext[k].divmod(row, q2, r);
+    const int j = (int)r - p.lo[k];
+    inside = inside && j >= 0 && j < p.sext[k];
+    so += (int64_t)j * p.sstr[k];
+    row = q2;
+  }
+}
+
+// 4 consecutive outputs per thread, 16-byte stores (n % 4 == 0): the outer index is decoded
+// once per inner-axis row the 4 outputs touch (once when the inner extent is a multiple of 4,
+// twice for the max-pool backward's 1 -> 2 interleave pads)
 __global__ void __launch_bounds__(256) pad_fast4(PadFast p, uint32_t value) {
   const uint32_t n4 = p.n >> 2;
   const int in = p.nd - 1;
+  const int E = (int)p.ext[in].d;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n4; q += gridDim.x * blockDim.x) {
-    uint32_t e = q << 2, qq, x;
-    p.ext[in].divmod(e, qq, x);
-    int64_t so = 0;
-    bool inside = true;
-    e = qq;
-    for (int k = in - 1; k >= 0; --k) {
-      uint32_t q2, r;
-      p.ext[k].divmod(e, q2, r);
-      int j = (int)r - p.lo[k];
-      inside = inside && j >= 0 && j < p.sext[k];
-      so += (int64_t)j * p.sstr[k];
-      e = q2;
-    }
+    uint32_t row, x0;
+    p.ext[in].divmod(q << 2, row, x0);
+    int64_t so;
+    bool inside;
+    pad_row(p, row, so, inside);
+    int x = (int)x0;
     uint32_t v[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int j = (int)x + u - p.lo[in];
+      if (x == E) {  // next inner-axis row
+        x = 0;
+        pad_row(p, ++row, so, inside);
+      }
+      const int j = x - p.lo[in];
       v[u] = (inside && j >= 0 && j < p.sext[in]) ? __ldg(p.src + so + (int64_t)j * p.sstr[in]) : value;
+      ++x;
     }
     reinterpret_cast<uint4*>(p.out)[q] = make_uint4(v[0], v[1], v[2], v[3]);
   }
@@ -1366,7 +1381,7 @@ static bool pad_fast_path(const pb_tensor* src, const int64_t* lo, const pb_scal
     int32_t i = scalar_as<int32_t>(value);
     memcpy(&bits, &i, 4);
   }
-  if (nd > 0 && oext[nd - 1] % 4 == 0 && out->ptr % 16 == 0)
+  if (nd > 0 && n % 4 == 0 && out->ptr % 16 == 0)
     pad_fast4<<<grid_for(n / 4, 256), 256, 0, compute_stream()>>>(p, bits);
   else
     pad_fast<<<grid_for(n, 1024), 256, 0, compute_stream()>>>(p, bits);

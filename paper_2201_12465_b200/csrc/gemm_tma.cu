@@ -673,10 +673,11 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
                  p->stride_h, p->stride_w, W, H * W};
     return run_conv(pr, gh, gl, wh, wl, o);
   }
-  if ((p->stride_h != 1 || p->stride_w != 1) && (int64_t)N * HO * WO <= 8192) {
+  if ((p->stride_h != 1 || p->stride_w != 1) && ((int64_t)N * HO * WO <= 8192 || Cx < 16)) {
     // strided k x k: Y = W^T g as a GEMM over the gradient pixels (rows) and the (c, r, s)
     // columns, then col2im gathers each dx pixel's on-grid taps.  Measured: wins up to
-    // N*HO*WO = 6272 (b32 at 14x14); at 28x28 the 9x-wide Y round trip loses to gemm_tc.cu.
+    // N*HO*WO = 6272 (b32 at 14x14) and for few input channels (the RGB stem: 0.67 vs 8 ms);
+    // at 28x28 the 9x-wide Y round trip loses to gemm_tc.cu.
     Prob pr = make_prob(N, HO, WO, F, 1, 1, 1, 1, 0, 0);
     const int RS = KH * KW;
     const int64_t act = (int64_t)N * F * HO * WO, rows = (int64_t)N * HO * WO, cols = (int64_t)Cx * RS;

@@ -214,6 +214,7 @@ class GpuBackend(Backend):
         # trace-planned fusion (fusion_trace_* / fusion_plan_*): a traced step tells which
         # elementwise results have exactly one consumer, itself elementwise; the planned
         # (captured) step keeps only those lazy, so no chain is ever computed twice
+        self._fills = None  # open fill cache: (dtype, type, value) -> one-element DevBlock
         self._trace = None
         self._plan = None
         self._planned = False
@@ -346,6 +347,15 @@ class GpuBackend(Backend):
             self._prod[id(res)] = (idx, weakref.ref(res))
         return res
 
+    def fill_cache_begin(self):
+        """Share full() blocks by value until fill_cache_end(); the caller keeps the returned
+        blocks alive for as long as anything recorded with them (a CUDA graph) may run."""
+        self._fills = {}
+
+    def fill_cache_end(self):
+        fills, self._fills = self._fills, None
+        return fills
+
     def fusion_trace_begin(self):
         """Record the op stream of one (eager) step: signatures and producer links."""
         self._trace, self._prod, self._op_idx = [], {}, 0
@@ -476,9 +486,20 @@ class GpuBackend(Backend):
                 raise OverflowError(f"Python integer {v} out of bounds for {dt.np}")
         if call.shape.size == 0:
             return DeviceArray(None, 0, shape, contig_strides(shape), dt)
-        blk = self._alloc(dt.itemsize, "full")
-        one = DeviceArray(blk, blk.ptr, (1,), (1,), dt)
-        _lib.check(self._lib.pb_fill(one.packed(), _lib.pack_scalar(call.params["value"])), "full")
+        # the one-element block behind a full() view is immutable, so while a fill cache is
+        # open (CapturedStep: traced warm-up + recording) equal fills share it -- the
+        # reference's sum backward creates one ones() per reduction (324 per ResNet-50
+        # step), each a 1-element kernel in the graph otherwise.  Blocks filled while a graph
+        # is being recorded only hold their value once the graph runs, so those are not shared.
+        fills = self._fills
+        key = (dt.name, type(v), v) if fills is not None and v == v else None  # NaN: not keyed
+        blk = fills.get(key) if key is not None else None
+        if blk is None:
+            blk = self._alloc(dt.itemsize, "full")
+            one = DeviceArray(blk, blk.ptr, (1,), (1,), dt)
+            _lib.check(self._lib.pb_fill(one.packed(), _lib.pack_scalar(call.params["value"])), "full")
+            if key is not None and not self._capture_pool and len(fills) < 4096:
+                fills[key] = blk
         return DeviceArray(blk, blk.ptr, shape, (0,) * len(shape), dt, fill=v)
 
     def _arange(self, call, args):

@@ -146,6 +146,8 @@ class CapturedStep:
             trace = self.fuse and self.calls == self.warmup
             if trace:
                 be.fusion_trace_begin()
+                if hasattr(be, "fill_cache_begin"):
+                    be.fill_cache_begin()  # closed after the recording (see _capture)
             try:
                 loss, out = self._body()
             finally:
@@ -192,5 +194,7 @@ class CapturedStep:
                     self._set(owner, key, before)
         finally:
             self.graph = be.capture_end()
+            if hasattr(be, "fill_cache_end"):
+                self._fills = be.fill_cache_end()  # blocks the graph reads: kept with it
         self.launches = be.launch_count() - n0  # kernels recorded into the graph (per replay)
         self.loss, self.out = loss, out
