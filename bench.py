@@ -305,7 +305,8 @@ def main():
             "roofline": roofline, "clocks": clk.summary(), "final_loss": final_loss,
             "gemm_path": {2: "tcgen05+tma", 1: "tcgen05", 0: "simt"}[be._lib.pb_gemm_path()],
             "step_mode": "cuda_graph" if step is not None else "eager", "eager": eager,
-            "fused_ops": step.fused_ops if step is not None else 0}
+            "fused_ops": step.fused_ops if step is not None else 0,
+            "plan_abandoned": step.plan_abandoned if step is not None else None}
     if graph_error:
         line["graph_error"] = graph_error
     if world == 1 and not args.no_cpu_baseline:

@@ -105,6 +105,10 @@ int pb_fill(const pb_tensor* out, const pb_scalar* value);                /* ker
 int pb_arange(const pb_tensor* out);                                      /* kernels.py:61-62 */
 int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out); /* kernels.py:65-74, rng.py */
 int pb_reduce(int op, const pb_tensor* a, int axis /* -1 = all */, const pb_tensor* out); /* :139-160 */
+/* pb_reduce then out = op(result, scalar) (or op(scalar, result)) in f32, op in add/sub/mul/div:
+   the reference's mean = sum / n (minml/ops.py:33-36) fused; backend-internal (planned fusion) */
+int pb_reduce_epi(int op, const pb_tensor* a, int axis, const pb_tensor* out, int epi_op, float scalar,
+                  int scalar_left);
 int pb_check(int what, const pb_tensor* a, int32_t* result); /* 0: any zero, 1: any negative (blocking) */
 int pb_matmul(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out); /* kernels.py:166-173 */
 typedef struct pb_conv {

@@ -94,7 +94,20 @@ struct RedArgs {
   int64_t st[PB_MAX_RANK];       // their strides in a
   FastDiv fd[PB_MAX_RANK];
   int64_t O, R, sR, chunk, chunks;
+  int epi, epi_left;  // f32 epilogue: out = op(result, s) or op(s, result); epi < 0: none
+  float epi_s;
 };
+
+// the f32 result, then the fused scalar op exactly as the elementwise kernel would apply it
+__device__ __forceinline__ float epilogue(const RedArgs& r, float v) {
+  const float a = r.epi_left ? r.epi_s : v, b = r.epi_left ? v : r.epi_s;
+  switch (r.epi) {
+    case PB_ADD: return a + b;
+    case PB_SUB: return a - b;
+    case PB_MUL: return a * b;
+    default: return a / b;
+  }
+}
 
 __device__ __forceinline__ int64_t out_base(const RedArgs& r, int64_t o) {
   int64_t off = 0;
@@ -152,6 +165,8 @@ __device__ __forceinline__ void emit(const RedArgs& r, int64_t o, int64_t c, typ
   }
   if (OP == PB_ARGMAX)
     reinterpret_cast<int64_t*>(r.out)[o] = acc.i < 0 ? 0 : acc.i;
+  else if (r.epi >= 0)
+    reinterpret_cast<float*>(r.out)[o] = epilogue(r, (float)acc.v);
   else
     store_from<typename Red<OP, T>::V>(r.out, r.dto, o, acc.v);
 }
@@ -326,15 +341,20 @@ __global__ void __launch_bounds__(256) red_final(RedArgs r) {
     for (int64_t c = 1; c < r.chunks; ++c) acc = RD::merge(acc, part[c * r.O + o]);
     if (OP == PB_ARGMAX)
       reinterpret_cast<int64_t*>(r.out)[o] = acc.i < 0 ? 0 : acc.i;
+    else if (r.epi >= 0)
+      reinterpret_cast<float*>(r.out)[o] = epilogue(r, (float)acc.v);
     else
       store_from<typename RD::V>(r.out, r.dto, o, acc.v);
   }
 }
 
 template <int OP, typename T>
-static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
+static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int epi, float epi_s, int epi_left) {
   typedef typename Red<OP, T>::Acc Acc;
   RedArgs r;
+  r.epi = epi;
+  r.epi_s = epi_s;
+  r.epi_left = epi_left;
   r.a = (const void*)(uintptr_t)a->ptr;
   r.out = (void*)(uintptr_t)out->ptr;
   r.dto = out->dtype;
@@ -374,6 +394,7 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
   for (int k = 0; k < r.nd && r.fast; ++k) r.fd[k] = FastDiv((uint32_t)r.shape[k]);
   if (r.O == 0) return PB_OK;
   if (r.R == 0) {  // empty sum -> zeros (max/min/argmax rejected by the planner)
+    if (epi >= 0) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_epi: empty reduction");
     pb_scalar z = {1, 0, 0.0, 0};
     return pb_fill(out, &z);
   }
@@ -443,14 +464,16 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out) {
 }
 
 template <int OP>
-static int dispatch(const pb_tensor* a, int axis, const pb_tensor* out) {
+static int dispatch(const pb_tensor* a, int axis, const pb_tensor* out, int epi = -1, float s = 0.f, int left = 0) {
+  if (epi >= 0 && (a->dtype != PB_F32 || out->dtype != PB_F32 || OP == PB_ARGMAX))
+    return fail(PB_ERR_UNSUPPORTED, "pb_reduce_epi: f32 sum/max/min only");
   switch (a->dtype) {
-    case PB_BOOL: return run_reduce<OP, bool>(a, axis, out);
-    case PB_U8: return run_reduce<OP, uint8_t>(a, axis, out);
-    case PB_I32: return run_reduce<OP, int32_t>(a, axis, out);
-    case PB_I64: return run_reduce<OP, int64_t>(a, axis, out);
-    case PB_F32: return run_reduce<OP, float>(a, axis, out);
-    case PB_F64: return run_reduce<OP, double>(a, axis, out);
+    case PB_BOOL: return run_reduce<OP, bool>(a, axis, out, epi, s, left);
+    case PB_U8: return run_reduce<OP, uint8_t>(a, axis, out, epi, s, left);
+    case PB_I32: return run_reduce<OP, int32_t>(a, axis, out, epi, s, left);
+    case PB_I64: return run_reduce<OP, int64_t>(a, axis, out, epi, s, left);
+    case PB_F32: return run_reduce<OP, float>(a, axis, out, epi, s, left);
+    case PB_F64: return run_reduce<OP, double>(a, axis, out, epi, s, left);
   }
   return fail(PB_ERR_ARG, "pb_reduce: bad dtype");
 }
@@ -467,4 +490,18 @@ extern "C" int pb_reduce(int op, const pb_tensor* a, int axis, const pb_tensor* 
     case PB_ARGMAX: return dispatch<PB_ARGMAX>(a, axis, out);
   }
   return fail(PB_ERR_ARG, "pb_reduce: unknown op");
+}
+
+// pb_reduce followed by an f32 scalar op on each result -- the reference's mean
+// (sum / n, minml/ops.py:33-36) in one launch; bit-identical to the two primitives
+extern "C" int pb_reduce_epi(int op, const pb_tensor* a, int axis, const pb_tensor* out, int epi_op, float scalar,
+                             int scalar_left) {
+  if (epi_op != PB_ADD && epi_op != PB_SUB && epi_op != PB_MUL && epi_op != PB_DIV)
+    return fail(PB_ERR_ARG, "pb_reduce_epi: epilogue must be add/sub/mul/div");
+  switch (op) {
+    case PB_SUM: return dispatch<PB_SUM>(a, axis, out, epi_op, scalar, scalar_left);
+    case PB_RMAX: return dispatch<PB_RMAX>(a, axis, out, epi_op, scalar, scalar_left);
+    case PB_RMIN: return dispatch<PB_RMIN>(a, axis, out, epi_op, scalar, scalar_left);
+  }
+  return fail(PB_ERR_ARG, "pb_reduce_epi: unknown op");
 }

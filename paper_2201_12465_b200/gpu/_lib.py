@@ -83,6 +83,7 @@ SIGNATURES = {
     "pb_arange": (_I, [_B]),
     "pb_rand": (_I, [_I, _U64, _U64, _B]),
     "pb_reduce": (_I, [_I, _B, _I, _B]),
+    "pb_reduce_epi": (_I, [_I, _B, _I, _B, _I, ctypes.c_float, _I]),
     "pb_check": (_I, [_I, _B, _I32P]),
     "pb_matmul": (_I, [_B, _B, _B]),
     "pb_conv2d": (_I, [_B, _B, _B, _B, _B]),

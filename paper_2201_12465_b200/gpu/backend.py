@@ -183,6 +183,50 @@ def compute_dtype(name, da, other, scalar):
 _INT_RANGE = {"u8": (0, 255), "i32": (-2**31, 2**31 - 1), "i64": (-2**63, 2**63 - 1)}
 
 
+class LazyReduce:
+    """Adapter of a deferred f32 reduction whose only consumer (per the traced plan) is a
+    scalar add/sub/mul/div: that consumer runs both as one ``pb_reduce_epi`` launch.  Any
+    other use runs the plain reduction first."""
+
+    __slots__ = ("be", "call", "arg", "shape", "strides", "dtype", "host", "_dev", "__weakref__")
+
+    def __init__(self, be, call, arg):
+        self.be, self.call, self.arg = be, call, arg
+        self.shape = tuple(call.shape)
+        self.strides = contig_strides(self.shape)
+        self.dtype = call.dtype
+        self.host = None
+        self._dev = None
+
+    def dev(self):
+        d = self._dev
+        if d is None:
+            d = self._dev = self.be._run_reduce(self.call, self.arg)
+            self.arg = None
+        return d
+
+    def materialize(self):
+        self.dev()
+
+    @property
+    def block(self):
+        return self.dev().block
+
+    @property
+    def ptr(self):
+        return self.dev().ptr
+
+    @property
+    def contiguous(self):
+        return True
+
+    def packed(self):
+        return self.dev().packed()
+
+
+_EPI = {"add", "sub", "mul", "div"}
+
+
 class GraphExec:
     """An instantiated CUDA graph of compute-stream work (see GpuBackend.capture_begin)."""
 
@@ -221,6 +265,7 @@ class GpuBackend(Backend):
         self._prod = {}
         self._op_idx = 0
         self._lazy_ok = True
+        self._lazy_red = False
         self._lib = _lib.load()
         _lib.check(self._lib.pb_init(device), "pb_init")
         self.device = device
@@ -312,7 +357,11 @@ class GpuBackend(Backend):
     def _execute(self, call, args):
         name = call.name
         if name not in _FUSE_BIN and name not in _FUSE_UN:
-            args = [a.dev() if type(a) is LazyArray else a for a in args]
+            args = [a.dev() if type(a) is LazyArray or type(a) is LazyReduce else a for a in args]
+        elif type(args[0]) is LazyReduce and not (name in _EPI and "scalar" in call.params):
+            args = [a.dev() if type(a) is LazyReduce else a for a in args]
+        elif len(args) > 1 and type(args[1]) is LazyReduce:
+            args = [a.dev() if type(a) is LazyReduce else a for a in args]
         ledger = self._manager if not isinstance(self._manager, MemoryManager) else None
         if ledger is not None:
             ledger.on_op_begin(call.name)
@@ -335,15 +384,17 @@ class GpuBackend(Backend):
         sig = (name, tuple(call.shape), call.dtype.name, tuple(tuple(a.shape) for a in args))
         prods = tuple(self._producer(a) for a in args)
         if self._trace is not None:
-            self._trace.append((sig, prods, fusible))
+            epi = name in _EPI and "scalar" in call.params and call.dtype is dtypes.f32
+            self._trace.append((sig, prods, fusible, epi))
         else:
-            tr, lazy = self._plan
+            tr, lazy, lazy_red = self._plan
             if idx < len(tr) and tr[idx][0] == sig and tr[idx][1] == prods:
                 self._lazy_ok = lazy[idx]
+                self._lazy_red = lazy_red[idx]
             else:  # the step diverged from the trace: stop fusing (everything materialises)
                 self._abandon_plan()
         res = self._execute(call, args)
-        if type(res) is DeviceArray or type(res) is LazyArray:
+        if type(res) is DeviceArray or type(res) is LazyArray or type(res) is LazyReduce:
             self._prod[id(res)] = (idx, weakref.ref(res))
         return res
 
@@ -365,15 +416,19 @@ class GpuBackend(Backend):
         consumed it exactly once, by an elementwise op.  Returns the number of such ops."""
         tr, self._trace, self._prod = self._trace, None, {}
         n = len(tr)
-        uses, by_fusible = [0] * n, [True] * n
-        for sig, prods, fusible in tr:
+        uses, by_fusible, by_epi = [0] * n, [True] * n, [True] * n
+        for sig, prods, fusible, epi in tr:
             for q in prods:
                 if q >= 0:
                     uses[q] += 1
                     by_fusible[q] = by_fusible[q] and fusible
+                    by_epi[q] = by_epi[q] and epi
         lazy = [tr[i][2] and uses[i] == 1 and by_fusible[i] for i in range(n)]
-        self._plan = (tr, lazy)
-        return sum(lazy)
+        # f32 sum/max/min whose one consumer is a scalar add/sub/mul/div (mean = sum / n)
+        lazy_red = [tr[i][0][0] in ("sum", "max_reduce", "min_reduce") and tr[i][0][2] == "f32" and
+                    uses[i] == 1 and by_epi[i] for i in range(n)]
+        self._plan = (tr, lazy, lazy_red)
+        return sum(lazy) + sum(lazy_red)
 
     def fusion_plan_begin(self):
         """Replay the planned step (normally while recording a CUDA graph): ops the plan marks
@@ -386,13 +441,20 @@ class GpuBackend(Backend):
 
     def _abandon_plan(self):
         self._lazy_ok = False
-        self._plan = ([], [])
+        self._lazy_red = False
+        self._plan = ([], [], [])
+
+    @property
+    def plan_abandoned(self):
+        """True when the planned step diverged from its trace (fusion stopped part-way)."""
+        return self._plan is not None and not self._plan[0]
 
     def fusion_plan_end(self):
         if self._planned:
             self._planned, self._prod = False, {}
             self._fuse = self._fuse_saved
         self._lazy_ok = True
+        self._lazy_red = False
 
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
@@ -653,6 +715,14 @@ class GpuBackend(Backend):
     def _binary(self, call, args):
         name = call.name
         p = call.params
+        if type(args[0]) is LazyReduce:
+            lr = args[0]
+            s = p["scalar"]
+            if (lr._dev is None and type(s) in (int, float) and call.dtype is dtypes.f32 and
+                    compute_dtype(name, lr.dtype, s, True) is dtypes.f32 and abs(float(s)) <= 3.4e38):
+                # (a later use of the plain reduction -- none per the plan -- would recompute it)
+                return self._run_reduce(lr.call, lr.arg, (name, float(s), p.get("scalar_side") == "left"))
+            args = [lr.dev()]
         if name == "mul" and "scalar" not in p:
             view = self._times_one(call, args)
             if view is not None:
@@ -706,6 +776,8 @@ class GpuBackend(Backend):
         spreads grads this way, minml/autograd.py:615-617): return a zero-copy view."""
         a, b = args
         for one, g in ((a, b), (b, a)):
+            if type(g) is LazyArray and type(one) is DeviceArray and one.fill is not None:
+                g = g.dev()  # run the (small) pending chain, then view it: never spread it
             if (type(one) is DeviceArray and one.fill is not None and type(g) is DeviceArray and
                     one.fill == 1 and type(one.fill) is not bool and g.dtype is call.dtype and
                     one.dtype is call.dtype and call.dtype.is_float):
@@ -746,7 +818,12 @@ class GpuBackend(Backend):
 
     # reductions
     def _reduce(self, call, args):
-        a = args[0]
+        if self._lazy_red and call.shape.size > 0 and args[0].dtype is dtypes.f32:
+            return LazyReduce(self, call, args[0])
+        return self._run_reduce(call, args[0])
+
+    def _run_reduce(self, call, a, epi=None):
+        """The reduction; with ``epi = (op, scalar, scalar_left)`` its f32 scalar consumer too."""
         out = self._new(tuple(call.shape), call.dtype, call.name)
         if out.block is None:
             return out
@@ -756,7 +833,12 @@ class GpuBackend(Backend):
             ax = -1
         else:
             ax = normalize_axis(axis, len(a.shape))
-        _lib.check(self._lib.pb_reduce(_lib.REDOP[call.name], a.packed(), ax, out.packed()), call.name)
+        if epi is None:
+            _lib.check(self._lib.pb_reduce(_lib.REDOP[call.name], a.packed(), ax, out.packed()), call.name)
+        else:
+            op, sc, left = epi
+            _lib.check(self._lib.pb_reduce_epi(_lib.REDOP[call.name], a.packed(), ax, out.packed(), _lib.BINOP[op],
+                                               sc, 1 if left else 0), call.name)
         return out
 
     # contractions

@@ -85,6 +85,7 @@ class CapturedStep:
         # step fuses every elementwise result whose single consumer is elementwise
         self.fuse = bool(fuse) and self.warmup >= 2 and hasattr(self.backend, "fusion_trace_begin")
         self.fused_ops = 0
+        self.plan_abandoned = None
         self.calls = 0
         self.graph = None
         self.x = self.y = None
@@ -171,6 +172,7 @@ class CapturedStep:
             finally:
                 if planned:
                     be.fusion_plan_end()
+                    self.plan_abandoned = be.plan_abandoned
         except BaseException:
             try:
                 be.capture_end()  # discard the partial recording

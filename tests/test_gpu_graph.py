@@ -64,6 +64,7 @@ def test_planned_fusion_bit_identical_and_fewer_launches(name, shape, classes):
     step = fused[4]
     assert step.fused_ops > 0 and step.launches < plain[4].launches, (step.fused_ops, step.launches,
                                                                      plain[4].launches)
+    assert step.plan_abandoned is False  # the recorded step followed its trace to the end
     assert eager[0] == fused[0], (eager[0], fused[0])
     for a, b in zip(eager[1] + eager[2] + eager[3], fused[1] + fused[2] + fused[3]):
         assert np.array_equal(a, b)
