@@ -56,6 +56,17 @@ int pb_synchronize(void);                /* wait for the compute stream */
 uint64_t pb_stream(int which);           /* 0 compute, 1 comm, 2 copy (cudaStream_t) */
 int pb_h2d(uint64_t dst, const void* src, uint64_t nbytes); /* pinned staging, async */
 int pb_d2h(void* dst, uint64_t src, uint64_t nbytes);       /* blocking */
+/* pipelined transfers (training.CapturedStep.run; the reference's read-ahead Prefetch,
+   minml/data.py:112-145): h2d through the pinned staging ring on stream `stream`
+   (0 compute, 2 copy); d2h posted into pinned slot 0..7 (<= 1 MiB) on the compute stream,
+   fetched later (waits for that copy only) */
+int pb_h2d_on(uint64_t dst, const void* src, uint64_t nbytes, int stream);
+int pb_d2h_post(uint64_t src, uint64_t nbytes, int slot);
+int pb_d2h_fetch(int slot, void* dst, uint64_t nbytes);
+/* page-locked host buffers: pb_h2d / pb_h2d_on DMA straight from them (no staging copy) */
+void* pb_host_alloc(uint64_t nbytes);   /* NULL on failure (pb_last_error) */
+int pb_host_free(void* p);
+int pb_stream_sync(int stream);          /* wait for one stream (0 compute, 1 comm, 2 copy) */
 int pb_d2d(uint64_t dst, uint64_t src, uint64_t nbytes);    /* async */
 int pb_event_record(int stream_from, int stream_to);        /* stream_to waits on stream_from */
 int pb_graph_begin(void);                 /* start capturing the compute stream */

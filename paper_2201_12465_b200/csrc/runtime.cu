@@ -109,6 +109,15 @@ static const int kStages = 4;
 static const size_t kStageBytes = (size_t)32 << 20;
 static Stage g_stage[kStages];
 static int g_stage_next = 0;
+// ---- posted device->host result slots ------------------------------------------------
+struct Post {
+  void* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  uint64_t bytes = 0;
+};
+static const int kPostSlots = 8;
+static const size_t kPostBytes = (size_t)1 << 20;
+static Post g_post[kPostSlots];
 
 }  // namespace pb
 
@@ -158,7 +167,18 @@ uint64_t pb_stream(int which) { return (uint64_t)(uintptr_t)g_streams[(which >= 
 
 uint64_t pb_launch_count(void) { return g_launches.load(); }
 
-int pb_h2d(uint64_t dst, const void* src, uint64_t nbytes) {
+int pb_h2d(uint64_t dst, const void* src, uint64_t nbytes) { return pb_h2d_on(dst, src, nbytes, 0); }
+
+int pb_h2d_on(uint64_t dst, const void* src, uint64_t nbytes, int stream) {
+  if (stream < 0 || stream > 2) return fail(PB_ERR_ARG, "pb_h2d_on: stream must be 0, 1 or 2");
+  if (nbytes == 0) return PB_OK;
+  cudaPointerAttributes attr;
+  if (cudaPointerGetAttributes(&attr, src) == cudaSuccess && attr.type == cudaMemoryTypeHost) {
+    // page-locked source (pb_host_alloc): one DMA, no staging copy on the host
+    PB_CUDA(cudaMemcpyAsync((void*)(uintptr_t)dst, src, nbytes, cudaMemcpyHostToDevice, g_streams[stream]));
+    return PB_OK;
+  }
+  cudaGetLastError();
   const char* s = (const char*)src;
   uint64_t off = 0;
   while (off < nbytes) {
@@ -167,8 +187,8 @@ int pb_h2d(uint64_t dst, const void* src, uint64_t nbytes) {
     if (st.pending) PB_CUDA(cudaEventSynchronize(st.ev));
     size_t len = (size_t)(nbytes - off) < st.cap ? (size_t)(nbytes - off) : st.cap;
     std::memcpy(st.host, s + off, len);
-    PB_CUDA(cudaMemcpyAsync((void*)(uintptr_t)(dst + off), st.host, len, cudaMemcpyHostToDevice, g_streams[0]));
-    PB_CUDA(cudaEventRecord(st.ev, g_streams[0]));
+    PB_CUDA(cudaMemcpyAsync((void*)(uintptr_t)(dst + off), st.host, len, cudaMemcpyHostToDevice, g_streams[stream]));
+    PB_CUDA(cudaEventRecord(st.ev, g_streams[stream]));
     st.pending = true;
     off += len;
   }
@@ -179,6 +199,50 @@ int pb_d2h(void* dst, uint64_t src, uint64_t nbytes) {
   if (nbytes == 0) return PB_OK;
   PB_CUDA(cudaMemcpyAsync(dst, (const void*)(uintptr_t)src, nbytes, cudaMemcpyDeviceToHost, g_streams[0]));
   PB_CUDA(cudaStreamSynchronize(g_streams[0]));
+  return PB_OK;
+}
+
+// posted device->host reads: a pinned slot per outstanding result, completed by an event, so
+// the host can read step i's loss while step i+1 is already queued behind it
+int pb_d2h_post(uint64_t src, uint64_t nbytes, int slot) {
+  if (slot < 0 || slot >= kPostSlots || nbytes > kPostBytes) return fail(PB_ERR_ARG, "pb_d2h_post: bad slot or size");
+  Post& p = g_post[slot];
+  if (!p.host) {
+    PB_CUDA(cudaHostAlloc(&p.host, kPostBytes, cudaHostAllocDefault));
+    PB_CUDA(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+  }
+  if (nbytes) PB_CUDA(cudaMemcpyAsync(p.host, (const void*)(uintptr_t)src, nbytes, cudaMemcpyDeviceToHost, g_streams[0]));
+  PB_CUDA(cudaEventRecord(p.ev, g_streams[0]));
+  p.bytes = nbytes;
+  return PB_OK;
+}
+
+void* pb_host_alloc(uint64_t nbytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, nbytes ? nbytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    set_error("pb_host_alloc: cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+int pb_host_free(void* p) {
+  if (p) PB_CUDA(cudaFreeHost(p));
+  return PB_OK;
+}
+
+int pb_stream_sync(int stream) {
+  if (stream < 0 || stream > 2) return fail(PB_ERR_ARG, "pb_stream_sync: stream must be 0, 1 or 2");
+  PB_CUDA(cudaStreamSynchronize(g_streams[stream]));
+  return PB_OK;
+}
+
+int pb_d2h_fetch(int slot, void* dst, uint64_t nbytes) {
+  if (slot < 0 || slot >= kPostSlots || !g_post[slot].host || nbytes > g_post[slot].bytes)
+    return fail(PB_ERR_ARG, "pb_d2h_fetch: slot not posted or size too large");
+  PB_CUDA(cudaEventSynchronize(g_post[slot].ev));
+  std::memcpy(dst, g_post[slot].host, nbytes);
   return PB_OK;
 }
 

@@ -58,6 +58,12 @@ SIGNATURES = {
     "pb_stream": (_U64, [_I]),
     "pb_h2d": (_I, [_U64, _P, _U64]),
     "pb_d2h": (_I, [_P, _U64, _U64]),
+    "pb_h2d_on": (_I, [_U64, _P, _U64, _I]),
+    "pb_d2h_post": (_I, [_U64, _U64, _I]),
+    "pb_d2h_fetch": (_I, [_I, _P, _U64]),
+    "pb_host_alloc": (_P, [_U64]),
+    "pb_host_free": (_I, [_P]),
+    "pb_stream_sync": (_I, [_I]),
     "pb_d2d": (_I, [_U64, _U64, _U64]),
     "pb_event_record": (_I, [_I, _I]),
     "pb_graph_begin": (_I, []),

@@ -23,7 +23,7 @@ import sys
 import numpy as np
 
 from .. import dtypes
-from ..errors import DeviceError, DomainError, DTypeError
+from ..errors import DeviceError, DomainError, DTypeError, OutOfMemory
 from ..memory import CachingManager, MemoryManager, op_tag
 from ..registry import Backend
 from ..shape import normalize_axis
@@ -503,6 +503,49 @@ class GpuBackend(Backend):
         _lib.check(self._lib.pb_h2d(a.ptr, host.ctypes.data, host.nbytes), "copy_in")
         if a.host is not None:
             a.host = host.copy()
+
+    def stage_in(self, tensor, host, stream=2):
+        """Like ``copy_in`` but on ``stream`` (2 = the copy stream) through the pinned
+        staging ring; order it against the compute stream with ``stream_wait``."""
+        a = tensor.adapter
+        host = np.ascontiguousarray(host, dtype=a.dtype.np)
+        if tuple(host.shape) != tuple(a.shape) or not a.contiguous or a.block is None:
+            raise ValueError("stage_in needs a dense device tensor of the same shape")
+        _lib.check(self._lib.pb_h2d_on(a.ptr, host.ctypes.data, host.nbytes, int(stream)), "stage_in")
+
+    def pinned(self, shape, dtype=np.float32):
+        """A numpy array in page-locked host memory (freed with the array): batches staged
+        here reach the device in one DMA, without the host copy into the staging ring."""
+        dt = np.dtype(dtype)
+        shape = tuple(int(d) for d in shape)
+        nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+        ptr = self._lib.pb_host_alloc(max(nbytes, 1))
+        if not ptr:
+            raise OutOfMemory(f"pinned host allocation of {nbytes} bytes failed")
+        buf = (ctypes.c_char * max(nbytes, 1)).from_address(ptr)
+        arr = np.frombuffer(buf, dtype=np.uint8, count=nbytes).view(dt).reshape(shape)
+        weakref.finalize(buf, self._lib.pb_host_free, ptr)
+        return arr
+
+    def stream_sync(self, stream):
+        _lib.check(self._lib.pb_stream_sync(int(stream)), "stream_sync")
+
+    def stream_wait(self, waiter, on):
+        """Stream ``waiter`` waits for the work enqueued so far on stream ``on``."""
+        _lib.check(self._lib.pb_event_record(int(on), int(waiter)), "stream_wait")
+
+    def post_read(self, tensor, slot):
+        """Enqueue an async device->host read of a dense tensor into pinned slot ``slot``."""
+        a = self._contig(tensor.adapter)
+        _lib.check(self._lib.pb_d2h_post(a.ptr, tensor.shape.size * a.dtype.itemsize, int(slot)), "post_read")
+        return (tuple(tensor.shape), a.dtype.np)
+
+    def fetch_read(self, slot, meta):
+        """Wait for the read posted in ``slot`` (only that copy) and return it as numpy."""
+        shape, dt = meta
+        out = np.empty(shape, dtype=dt)
+        _lib.check(self._lib.pb_d2h_fetch(int(slot), out.ctypes.data, out.nbytes), "fetch_read")
+        return out
 
     def copy_device(self, dst, src):
         """dst <- src for two dense same-shaped device tensors (stream-ordered, capturable)."""

@@ -91,6 +91,7 @@ class CapturedStep:
         self.x = self.y = None
         self.loss = self.out = None
         self.launches = 0
+        self._stage = None
 
     def _slots(self):
         slots = []
@@ -159,6 +160,55 @@ class CapturedStep:
             self._capture()
         self.graph.launch()
         return self.loss.scalar(), self.out
+
+    def run(self, batches):
+        """Pipelined steps over an iterable of host ``(images, labels)`` batches; yields each
+        step's loss as a float, in order (the reference's ``train_step`` loop with its
+        read-ahead ``Prefetch``, minml/data.py:112-145, moved to the device queue).
+
+        Once the graph is recorded, batch i+1's host->device copy runs on the copy stream
+        while step i computes, and step i's loss comes back through a posted pinned read
+        that the host collects after queueing step i+1, so the compute stream never waits
+        for the host.  Every step still copies its whole batch in and its loss out.  Batches
+        in page-locked memory (``GpuBackend.pinned``) go over in one DMA; a batch's host
+        buffers may be reused once the loss of the step before it has been yielded.
+        """
+        be = self.backend
+        pending, k = None, 0
+        for images, labels in batches:
+            if self.graph is None:
+                yield self(images, labels)[0]
+                continue
+            labels = np.asarray(labels)
+            classes = self.out.shape[1]
+            if labels.size and (labels.min() < 0 or labels.max() >= classes):
+                bad = labels[(labels < 0) | (labels >= classes)][0]
+                raise IndexError(f"target {int(bad)} out of range for {classes} classes")
+            if self._stage is None:  # two dense device slots per input, written by the copy stream
+                self._stage = [(T.tensor(np.zeros(tuple(self.x.shape), self.x.dtype.np), backend=be.name),
+                                T.tensor(np.zeros(tuple(self.y.shape), self.y.dtype.np), backend=be.name))
+                               for _ in range(2)]
+            sx, sy = self._stage[k % 2]
+            be.stage_in(sx, images, stream=2)
+            be.stage_in(sy, labels, stream=2)
+            be.stream_wait(0, 2)  # compute waits for this batch
+            be.copy_device(self.x, sx)
+            be.copy_device(self.y, sy)
+            be.stream_wait(2, 0)  # the next copy into this slot waits for these reads
+            self.calls += 1
+            self.graph.launch()
+            loss = self.loss.data if isinstance(self.loss, Variable) else self.loss
+            meta = be.post_read(loss, k % 8)
+            if pending is not None:
+                value = float(be.fetch_read(*pending).reshape(()))
+                # step k-1 is done, so this batch's copy (queued behind it) is about to land:
+                # wait for it, then the caller may reuse the host buffers of this batch
+                be.stream_sync(2)
+                yield value
+            pending = (k % 8, meta)
+            k += 1
+        if pending is not None:
+            yield float(be.fetch_read(*pending).reshape(()))
 
     def _capture(self):
         be = self.backend
