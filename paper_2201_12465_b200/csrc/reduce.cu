@@ -260,10 +260,35 @@ __global__ void __launch_bounds__(256) red_rows(RedArgs r, int rows_per_block, i
     if (vec) {  // o0 * R % 4 == 0 and the base is 16-byte aligned
       const int n4 = n >> 2;
       const float4* s4 = reinterpret_cast<const float4*>(src);
-      for (int q = threadIdx.x; q < n4; q += blockDim.x) rows_smem4[q] = __ldg(s4 + q);
+      // 4 loads in flight per thread before any shared-memory store
+      for (int q0 = threadIdx.x; q0 < n4; q0 += 4 * blockDim.x) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * blockDim.x;
+          if (q < n4) v[u] = __ldg(s4 + q);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * blockDim.x;
+          if (q < n4) rows_smem4[q] = v[u];
+        }
+      }
       e0 = n4 << 2;
     }
-    for (int e = e0 + threadIdx.x; e < n; e += blockDim.x) buf[e] = src[e];
+    for (int e0b = e0 + threadIdx.x; e0b < n; e0b += 4 * blockDim.x) {
+      T v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0b + u * blockDim.x;
+        if (e < n) v[u] = src[e];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = e0b + u * blockDim.x;
+        if (e < n) buf[e] = v[u];
+      }
+    }
     __syncthreads();
     if ((int)threadIdx.x < rows) {
       const int t = threadIdx.x;
@@ -327,6 +352,47 @@ __global__ void __launch_bounds__(256) red_cols(RedArgs r) {
       emit<OP, T>(r, o, 0, acc);
     }
     __syncthreads();
+  }
+}
+
+// f32 sum over a strided axis whose innermost kept axis is contiguous (extent % 4 == 0, every
+// stride % 4 == 0, 16-byte aligned base): each thread owns 4 consecutive outputs and walks the
+// whole reduced axis with float4 loads, 8 in flight (a warp reads 512 contiguous bytes per
+// load), summing each output in f64 in index order.  No shared memory, no block barrier.
+// This is the reference's _unbroadcast sum(0) over [N, C, H, W] (minml/autograd.py:290-297).
+__global__ void __launch_bounds__(256) red_cols4_sum(RedArgs r) {
+  const float* a = (const float*)r.a;
+  const int64_t O4 = r.O >> 2, R = r.R, sR = r.sR;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < O4; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = q << 2;
+    const float* p = a + out_base(r, o);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    int64_t j = 0;
+    for (; j + 8 <= R; j += 8) {
+      float4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(p + (j + u) * sR));
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        s0 += (double)v[u].x;
+        s1 += (double)v[u].y;
+        s2 += (double)v[u].z;
+        s3 += (double)v[u].w;
+      }
+    }
+    for (; j < R; ++j) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(p + j * sR));
+      s0 += (double)v.x;
+      s1 += (double)v.y;
+      s2 += (double)v.z;
+      s3 += (double)v.w;
+    }
+    typedef Red<PB_SUM, float>::Acc Acc;
+    Acc c0{s0, -1}, c1{s1, -1}, c2{s2, -1}, c3{s3, -1};
+    emit<PB_SUM, float>(r, o, 0, c0);
+    emit<PB_SUM, float>(r, o + 1, 0, c1);
+    emit<PB_SUM, float>(r, o + 2, 0, c2);
+    emit<PB_SUM, float>(r, o + 3, 0, c3);
   }
 }
 
@@ -405,7 +471,7 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int ep
     r.chunks = 1;
     r.chunk = r.R;
     r.partial = nullptr;
-    const int rows = r.R <= 32 ? 256 : 128;
+    const int rows = r.R <= 32 ? 256 : r.R <= 64 ? 128 : 64;
     const size_t smem = (size_t)rows * r.R * 4;
     static bool attr = false;
     if (!attr) {
@@ -420,6 +486,23 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int ep
     red_rows<OP, T><<<grid, 256, smem, s>>>(r, rows, vec);
     PB_LAUNCHED();
     return PB_OK;
+  }
+  if (OP == PB_SUM && std::is_same<T, float>::value && r.sR > 1 && r.sR % 4 == 0 && r.nd >= 1 &&
+      r.st[r.nd - 1] == 1 && r.shape[r.nd - 1] % 4 == 0 && ((uintptr_t)r.a) % 16 == 0 && r.R <= 4096 &&
+      (r.O >= 4096 || r.R <= 64)) {
+    bool ok = true;
+    for (int k = 0; k + 1 < r.nd; ++k) ok = ok && r.st[k] % 4 == 0;
+    if (ok) {
+      r.chunks = 1;
+      r.chunk = r.R;
+      r.partial = nullptr;
+      const int64_t threads = r.O / 4;
+      const int64_t blocks = (threads + 255) / 256;
+      const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+      red_cols4_sum<<<grid, 256, 0, s>>>(r);
+      PB_LAUNCHED();
+      return PB_OK;
+    }
   }
   if (r.sR > 1 && r.R <= 4096) {
     r.chunks = 1;

@@ -18,6 +18,20 @@ rng = np.random.default_rng(0)
 x = Variable(T.tensor(rng.standard_normal((32, 3, 224, 224)).astype(np.float32), backend=be.name))
 y = T.tensor(rng.integers(0, 1000, 32).astype(np.int64), backend=be.name)
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+if len(sys.argv) > 2 and sys.argv[2] == "graph":
+    # captured step (fused plan): warm-up + record, then ONE replay -- the last
+    # launches_per_step kernels of an ncu launch list over this command are that replay
+    from paper_2201_12465_b200 import training
+    xh = rng.standard_normal((32, 3, 224, 224)).astype(np.float32)
+    yh = rng.integers(0, 1000, 32).astype(np.int64)
+    step = training.CapturedStep(model, opt, warmup=2)
+    for _ in range(3):
+        step(xh, yh)
+    be.synchronize()
+    step.graph.launch()
+    be.synchronize()
+    print("graph launches per step", step.launches)
+    sys.exit(0)
 for _ in range(steps):
     opt.zero_grad()
     loss = nn.cross_entropy(model(x), y)
