@@ -1,10 +1,14 @@
 """The measured unit of work: one optimizer step (semantics of minml/training.py:30-51)."""
 
+import json
+import struct
+
 import numpy as np
 
 from . import _tensor as T
-from . import nn, registry
+from . import nn, optim, registry
 from .autograd import Variable
+from .errors import FormatError
 
 
 def model_backend(model):
@@ -250,3 +254,86 @@ class CapturedStep:
                 self._fills = be.fill_cache_end()  # blocks the graph reads: kept with it
         self.launches = be.launch_count() - n0  # kernels recorded into the graph (per replay)
         self.loss, self.out = loss, out
+
+
+# ---------------------------------------------------------------------- checkpoints
+# The reference's checkpoint container (minml/training.py:119-214): "MNCK", u32 version, a
+# JSON header (epoch, the backend's RNG counter state, optimizer recipe, extra), the
+# serialized model (nn.serialize), then the optimizer's state arrays.  Device tensors are
+# read through to_host, so a checkpoint written on the GPU loads bit-exactly into the CPU
+# reference and vice versa.  Restore order: model first (constructors draw from the RNG),
+# then restore_rng, so a resumed run consumes the counter sequence of the uninterrupted one.
+
+CHECKPOINT_MAGIC = b"MNCK"
+CHECKPOINT_VERSION = 1
+_OPTIMIZER_KINDS = {
+    "sgd": (optim.SGD, ("lr", "momentum", "weight_decay")),
+    "adam": (optim.Adam, ("lr", "beta1", "beta2", "eps", "weight_decay")),
+}
+
+
+def _optimizer_kind(optimizer):
+    for kind, (cls, _) in _OPTIMIZER_KINDS.items():
+        if type(optimizer) is cls:
+            return kind
+    raise FormatError(f"cannot checkpoint optimizer type {type(optimizer).__name__}")
+
+
+class Checkpoint:
+    """What load_checkpoint returns; restore_optimizer / restore_rng rebuild the rest."""
+
+    def __init__(self, model, epoch, rng_state, optimizer_recipe, optimizer_arrays, extra):
+        self.model, self.epoch, self.rng_state = model, epoch, rng_state
+        self.optimizer_recipe, self.optimizer_arrays, self.extra = optimizer_recipe, optimizer_arrays, extra
+
+    def restore_optimizer(self, params=None):
+        if self.optimizer_recipe is None:
+            raise FormatError("checkpoint was saved without optimizer state")
+        cls, _ = _OPTIMIZER_KINDS[self.optimizer_recipe["kind"]]
+        opt = cls(self.model.params() if params is None else params, **self.optimizer_recipe["hyper"])
+        opt.load_state_config(self.optimizer_recipe["config"])
+        opt.load_state_entries(dict(self.optimizer_arrays))
+        return opt
+
+    def restore_rng(self, backend=None):
+        be = registry.default() if backend is None else registry.get(backend)
+        be.rng.restore(self.rng_state)
+
+
+def save_checkpoint(path, model, optimizer=None, epoch=0, extra=None):
+    be = registry.get(model_backend(model))
+    header = {"epoch": int(epoch), "rng": be.rng.state(), "extra": extra or {}}
+    if optimizer is not None:
+        kind = _optimizer_kind(optimizer)
+        header["optimizer"] = {"kind": kind,
+                               "hyper": {f: getattr(optimizer, f) for f in _OPTIMIZER_KINDS[kind][1]},
+                               "config": optimizer.state_config()}
+    buf = bytearray(CHECKPOINT_MAGIC)
+    buf += struct.pack("<I", CHECKPOINT_VERSION)
+    nn._w_str(buf, json.dumps(header, sort_keys=True))
+    blob = nn.serialize(model)
+    buf += struct.pack("<Q", len(blob)) + blob
+    entries = optimizer.state_entries() if optimizer is not None else []
+    buf += struct.pack("<I", len(entries))
+    for name, array in entries:
+        nn._w_array(buf, name, array)
+    with open(path, "wb") as f:
+        f.write(bytes(buf))
+
+
+def load_checkpoint(path, backend=None):
+    with open(path, "rb") as f:
+        raw = f.read()
+    r = nn._Reader(raw)
+    if bytes(r.take(4)) != CHECKPOINT_MAGIC:
+        raise FormatError("not a checkpoint (bad magic)", offset=0)
+    version = r.u32()
+    if version != CHECKPOINT_VERSION:
+        raise FormatError(f"unsupported checkpoint version {version}", offset=4)
+    header = json.loads(r.string())
+    model = nn.deserialize(bytes(r.take(r.u64())), backend=backend)
+    arrays = [r.array() for _ in range(r.u32())]
+    if r.pos != len(raw):
+        raise FormatError(f"{len(raw) - r.pos} trailing bytes", offset=r.pos)
+    return Checkpoint(model, header["epoch"], header["rng"], header.get("optimizer"), arrays,
+                      header.get("extra", {}))
