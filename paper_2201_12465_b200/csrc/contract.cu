@@ -11,6 +11,7 @@ int pb_conv2d_grad_input_simt(const pb_tensor* g, const pb_tensor* w, const pb_c
 int pb_conv2d_grad_weight_simt(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
 // tensor-core path: returns PB_ERR_UNSUPPORTED (without side effects) when it declines
 int pb_matmul_tc(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out);
+int pb_matmul_tma(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out);
 int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_input_tc(const pb_tensor* g, const pb_tensor* w, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_weight_tc(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
@@ -31,6 +32,10 @@ int pb_set_gemm_path(int path) {
 }
 
 int pb_matmul(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
+  if (g_tc == 2) {
+    int rc = pb_matmul_tma(a, b, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
+  }
   if (g_tc) {
     int rc = pb_matmul_tc(a, b, out);
     if (rc != PB_ERR_UNSUPPORTED) return rc;

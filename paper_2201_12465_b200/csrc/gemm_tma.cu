@@ -169,6 +169,7 @@ struct Prob {
   FastDiv fKB;         // wgrad: k-blocks per image
   int ti, tj, ntiles, zdim;
   FastDiv fP, fWO;     // output pixel decode (ho*wo, wo)
+  int plain;           // 1x1, stride 1, no padding: A is a plain [pixels][C] plane (tiled TMA)
 };
 
 template <int BN, bool WG>
@@ -274,6 +275,9 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
       const int z = t / per_z, split = z / (pr.KH * pr.KW);
       kbeg = split * pr.kper;
       kend = min(pr.K, kbeg + pr.kper);
+    } else if (pr.zdim > 1) {  // plain GEMM with split K: z = split
+      kbeg = (t / per_z) * pr.kper;
+      kend = min(pr.K, kbeg + pr.kper);
     } else {
       kbeg = 0;
       kend = pr.K;
@@ -311,8 +315,13 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
             const int tap = kb / cblocks, c0 = (kb - tap * cblocks) * BK;
             const int r = tap / pr.KW, sx = tap - r * pr.KW;
             const int wc = wo * pr.SW - pr.PW, hc = ho * pr.SH - pr.PH;
-            tma_im2col(base, &xa_hi, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
-            tma_im2col(base + C::A_BYTES, &xa_lo, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
+            if (pr.plain) {  // [rows][K] planes: the k-block is simply k0
+              tma_2d(base, &xa_hi, &full[s], k0, i0);
+              tma_2d(base + C::A_BYTES, &xa_lo, &full[s], k0, i0);
+            } else {
+              tma_im2col(base, &xa_hi, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
+              tma_im2col(base + C::A_BYTES, &xa_lo, &full[s], c0, wc, hc, n, (uint16_t)sx, (uint16_t)r);
+            }
             tma_2d(base + 2 * C::A_BYTES, &b_hi, &full[s], k0, j0);
             tma_2d(base + 2 * C::A_BYTES + C::B_BYTES, &b_lo, &full[s], k0, j0);
           } else {
@@ -500,6 +509,36 @@ __global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi
   }
 }
 
+// strided view v(r, k) = src[r * sr + k * sk] -> hi/lo[r][k] with row pitch kp (k >= K: 0),
+// a 32x32 tile per block through shared memory; loads run along whichever axis is unit stride
+__global__ void __launch_bounds__(256) kmajor_split(const float* __restrict__ src, float* __restrict__ hi,
+                                                    float* __restrict__ lo, int R, int K, int kp, int64_t sr,
+                                                    int64_t sk) {
+  __shared__ float t[32][33];
+  const int r0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const bool along_r = sk != 1 && sr == 1;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = ty + 8 * q;  // the slow index of this load
+    const int r = along_r ? r0 + tx : r0 + a, k = along_r ? k0 + a : k0 + tx;
+    const float v = r < R && k < K ? __ldg(src + (int64_t)r * sr + (int64_t)k * sk) : 0.f;
+    if (along_r) t[tx][a] = v;
+    else t[a][tx] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rr = ty + 8 * q, r = r0 + rr, k = k0 + tx;
+    if (r < R && k < kp) {
+      float h, l;
+      split_hl(t[rr][tx], h, l);
+      hi[(int64_t)r * kp + k] = h;
+      lo[(int64_t)r * kp + k] = l;
+    }
+  }
+}
+
 // strided dgrad, second half: dx[n][c][h][w] = sum over the taps (r, s) that land on the
 // stride grid of Y[(c, r, s)][(n, ho, wo)], ho = (h + ph - r) / sh; taps in (r, s) order, f64
 __global__ void __launch_bounds__(256) col2im_dgrad(const float* __restrict__ Y, float* __restrict__ dx, int N, int C,
@@ -577,9 +616,17 @@ template <class OUT>
 static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh, const float* wl, const OUT& o) {
   CUtensorMap ah, al, bh, bl;
   const int BN = pr.Nj <= 64 ? 64 : 128;  // (128-wide tiles win even with a ragged last wave)
-  if (!map_im2col(&ah, xh, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM) ||
-      !map_im2col(&al, xl, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM) ||
-      !map_2d(&bh, wh, pr.K, pr.Nj, BN) || !map_2d(&bl, wl, pr.K, pr.Nj, BN))
+  static int plain_ok = -1;  // experiment hook: PB_TMA_PLAIN=0 keeps 1x1 convs on im2col boxes
+  if (plain_ok < 0) {
+    const char* e = getenv("PB_TMA_PLAIN");
+    plain_ok = !(e && e[0] == '0');
+  }
+  pr.plain = plain_ok && pr.KH == 1 && pr.KW == 1 && pr.SH == 1 && pr.SW == 1 && pr.PH == 0 && pr.PW == 0;
+  const int64_t pix = (int64_t)pr.N * pr.H * pr.W;
+  bool ok = pr.plain ? map_2d(&ah, xh, pr.C, pix, BM) && map_2d(&al, xl, pr.C, pix, BM)
+                     : map_im2col(&ah, xh, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM) &&
+                           map_im2col(&al, xl, pr.N, pr.H, pr.W, pr.C, pr.KH, pr.KW, pr.SH, pr.SW, pr.PH, pr.PW, BM);
+  if (!ok || !map_2d(&bh, wh, pr.K, pr.Nj, BN) || !map_2d(&bl, wl, pr.K, pr.Nj, BN))
     return fail(PB_ERR_CUDA, "tma conv: tensor map encoding failed");
   pr.zdim = 1;
   if (BN == 64) return launch<64, false>(ah, al, bh, bl, pr, o);
@@ -817,6 +864,72 @@ int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* gr, const pb_
   if (rc || splits == 1) return rc;
   OutMat fin{dw, C * RS, F, (int64_t)C * RS, 0};
   fold_partials<OutMat><<<grid_for((int64_t)C * RS * F, 256), 256, 0, compute_stream()>>>(part, splits, C * RS, F, fin);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+// rank-2 matmul C[m][n] = sum_k A[m][k] B[k][n] (minml/kernels.py:166-173) as the plain
+// TMA GEMM D[i = n][j = m]: both operands go through kmajor_split (any strides, so the
+// autograd's transposed views need no copy) into [rows][kp] planes; split K over z when the
+// tile grid is short of the SM count, partials folded in f64 in split order
+int pb_matmul_tma(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) {
+  if (!g_tma || !driver_ok()) return PB_ERR_UNSUPPORTED;
+  if (a->ndim != 2 || b->ndim != 2 || a->dtype != PB_F32 || b->dtype != PB_F32 || out->dtype != PB_F32 ||
+      !is_contiguous(*out))
+    return PB_ERR_UNSUPPORTED;
+  const int64_t M = a->shape[0], K = a->shape[1], N = b->shape[1];
+  // measured in CUDA graphs (tools/mm_table.py): the operand pre-pass pays off once M >= 256;
+  // for the b128 classifier GEMMs (M = 128, multi-MB weights) gemm_tc.cu's in-GEMM split wins
+  if (M < 256 || N < 64 || K < 64 || !fits(M * N) || !fits(M * K) || !fits(N * K)) return PB_ERR_UNSUPPORTED;
+  const int64_t kp = (K + 3) / 4 * 4;
+  const int BN = M <= 64 ? 64 : 128;
+  Prob pr{};
+  pr.plain = 1;
+  pr.Mi = (int)N;
+  pr.Nj = (int)M;
+  pr.K = (int)kp;
+  pr.C = (int)kp;
+  pr.KH = pr.KW = pr.SH = pr.SW = 1;
+  const int64_t tiles = ((N + BM - 1) / BM) * ((M + BN - 1) / BN);
+  const int64_t kblocks = (kp + BK - 1) / BK;
+  int splits = 1;
+  if (tiles < num_sms()) {
+    splits = (int)(num_sms() / tiles);
+    if (splits > kblocks / 4) splits = (int)(kblocks / 4);
+    if (splits < 1) splits = 1;
+  }
+  int per = (int)((kblocks + splits - 1) / splits) * BK;
+  splits = (int)((kp + per - 1) / per);
+  pr.kper = per;
+  pr.zdim = splits;
+  const size_t nb = ((size_t)N * kp * 4 + 1023) / 1024 * 1024, mb = ((size_t)M * kp * 4 + 1023) / 1024 * 1024;
+  const size_t part = splits > 1 ? (size_t)splits * M * N * 4 : 0;
+  char* ws = (char*)workspace(2 * nb + 2 * mb + part);
+  if (!ws) return fail(PB_ERR_OOM, "matmul (tma): no workspace");
+  float *nh = (float*)ws, *nl = (float*)(ws + nb), *mh = (float*)(ws + 2 * nb), *ml = (float*)(ws + 2 * nb + mb);
+  float* pw = (float*)(ws + 2 * nb + 2 * mb);
+  cudaStream_t s = compute_stream();
+  // rows n of D: B^T, v(n, k) = B[k][n]; rows m: v(m, k) = A[m][k]
+  kmajor_split<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((N + 31) / 32)), 256, 0, s>>>(
+      (const float*)(uintptr_t)b->ptr, nh, nl, (int)N, (int)K, (int)kp, b->strides[1], b->strides[0]);
+  PB_LAUNCHED();
+  kmajor_split<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((M + 31) / 32)), 256, 0, s>>>(
+      (const float*)(uintptr_t)a->ptr, mh, ml, (int)M, (int)K, (int)kp, a->strides[0], a->strides[1]);
+  PB_LAUNCHED();
+  CUtensorMap ah, al, bh, bl;
+  if (!map_2d(&ah, nh, kp, N, BM) || !map_2d(&al, nl, kp, N, BM) || !map_2d(&bh, mh, kp, M, BN) ||
+      !map_2d(&bl, ml, kp, M, BN))
+    return fail(PB_ERR_CUDA, "matmul (tma): tensor map encoding failed");
+  float* c = (float*)(uintptr_t)out->ptr;
+  if (splits == 1) {
+    OutMat o{c, (int)N, (int)M, N, 0};
+    return BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, o) : launch<128, false>(ah, al, bh, bl, pr, o);
+  }
+  OutPartial op{pw, (int)N, (int)M};
+  int rc = BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, op) : launch<128, false>(ah, al, bh, bl, pr, op);
+  if (rc) return rc;
+  OutMat fin{c, (int)N, (int)M, N, 0};
+  fold_partials<OutMat><<<grid_for(M * N, 256), 256, 0, s>>>(pw, splits, (int)N, (int)M, fin);
   PB_LAUNCHED();
   return PB_OK;
 }

@@ -5,6 +5,7 @@ Descriptors cross the boundary as packed bytes laid out exactly like ``pb_tensor
 ctypes.Structure).  Any nonzero status raises ``DeviceError`` carrying pb_last_error().
 """
 
+import atexit
 import ctypes
 import os
 import struct
@@ -114,6 +115,21 @@ SIGNATURES = {
 _lib = None
 
 
+def _at_exit():
+    """Interpreter exit: drain the device, then detach the library so the finalizers of
+    device blocks and graphs that module teardown runs later (DevBlock, GraphExec) become
+    no-ops instead of calling into a CUDA runtime that is shutting down -- a process that
+    still held a recorded graph's pool could hang there.  The driver reclaims everything."""
+    global _lib
+    lib = _lib
+    if lib is not None:
+        try:
+            lib.pb_synchronize()
+        except Exception:  # noqa: BLE001
+            pass
+    _lib = None
+
+
 def load():
     """Load the shared library once (raises OSError if it is missing)."""
     global _lib
@@ -124,6 +140,7 @@ def load():
             fn.restype = res
             fn.argtypes = args
         _lib = lib
+        atexit.register(_at_exit)
     return _lib
 
 
