@@ -151,3 +151,30 @@ def test_tc_matches_simt_path(gpu):
         for a, b in zip(outs[:n], other):
             for u, v in zip(a, b):
                 assert rel_err(u, v) <= TOL
+
+
+@pytest.mark.parametrize("m,k,n", [(256, 96, 80), (300, 770, 130), (2048, 768, 64), (256, 2048, 96), (512, 67, 257)])
+def test_tma_matmul_matches_f64_reference(gpu, m, k, n):
+    """pb_matmul_tma (rank 2, M >= 256: operands pre-split into K-major planes from any
+    strided view, split-K folded in f64) against the reference's f64 product
+    (minml/kernels.py:166-173), for the three operand layouts the autograd issues: x @ W^T,
+    g @ W and g^T @ x.  Shapes cover ragged K (padded pitch, zero tails), ragged M/N tiles and
+    the split-K path (few tiles, long K)."""
+    r = np.random.default_rng(m + k + n)
+    a = r.standard_normal((m, k)).astype(np.float32)
+    w = (r.standard_normal((n, k)) / np.sqrt(k)).astype(np.float32)
+    ta = T.tensor(a, backend=gpu.name)
+    tw = T.tensor(w, backend=gpu.name)
+    launches0 = gpu.launch_count()
+    got = T.matmul(ta, tw.transpose()).to_host_buffer()              # W^T as a strided view
+    assert gpu.launch_count() - launches0 >= 3                         # 2 pre-passes + the GEMM
+    want = (a.astype(np.float64) @ w.astype(np.float64).T).astype(np.float32)
+    assert rel_err(got, want) <= TOL
+    g = r.standard_normal((m, n)).astype(np.float32)
+    tg = T.tensor(g, backend=gpu.name)
+    got = T.matmul(tg, tw).to_host_buffer()                            # [m,n] x [n,k]
+    assert rel_err(got, (g.astype(np.float64) @ w.astype(np.float64)).astype(np.float32)) <= TOL
+    if k >= 256:
+        got = T.matmul(tg.transpose(), ta).to_host_buffer()           # [n,m] x [m,k], M = n
+        want = (g.astype(np.float64).T @ a.astype(np.float64)).astype(np.float32)
+        assert rel_err(got, want) <= TOL
