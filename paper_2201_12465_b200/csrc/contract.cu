@@ -12,6 +12,7 @@ int pb_conv2d_grad_weight_simt(const pb_tensor* x, const pb_tensor* g, const pb_
 // tensor-core path: returns PB_ERR_UNSUPPORTED (without side effects) when it declines
 int pb_matmul_tc(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out);
 int pb_matmul_tma(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out);
+int pb_conv2d_grad_weight_mm(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_input_tc(const pb_tensor* g, const pb_tensor* w, const pb_conv* p, const pb_tensor* out);
 int pb_conv2d_grad_weight_tc(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out);
@@ -68,6 +69,10 @@ int pb_conv2d_grad_input(const pb_tensor* g, const pb_tensor* w, const pb_conv* 
 }
 
 int pb_conv2d_grad_weight(const pb_tensor* x, const pb_tensor* g, const pb_conv* p, const pb_tensor* out) {
+  if (g_tc == 2) {
+    int rc = pb_conv2d_grad_weight_mm(x, g, p, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
+  }
   if (g_tc == 2) {
     int rc = pb_conv2d_grad_weight_tma(x, g, p, out);
     if (rc != PB_ERR_UNSUPPORTED) return rc;

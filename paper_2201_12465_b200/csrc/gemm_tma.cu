@@ -539,6 +539,44 @@ __global__ void __launch_bounds__(256) kmajor_split(const float* __restrict__ sr
   }
 }
 
+// the operand planes of a 1x1 wgrad: v(r, k) = src[r * sr + n * sn + ho * sh + wo * sw] with
+// k = (n, ho, wo) over an N x HO x WO grid -> hi/lo[r][k], row pitch kp (k >= K: 0).  Lanes run
+// along k (consecutive wo), so loads are unit-stride (stride 1) or every other float (stride 2).
+__global__ void __launch_bounds__(256) kmajor_split_grid(const float* __restrict__ src, float* __restrict__ hi,
+                                                         float* __restrict__ lo, int R, int K, int kp, int64_t sr,
+                                                         int64_t sn, int64_t sh, int64_t sw, FastDiv fP, FastDiv fWO) {
+  const int r0 = blockIdx.y * 8, k = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int r = r0 + (threadIdx.x >> 5);
+  if (r >= R || k >= kp) return;
+  float h = 0.f, l = 0.f;
+  if (k < K) {
+    uint32_t n, q, ho, wo;
+    fP.divmod((uint32_t)k, n, q);
+    fWO.divmod(q, ho, wo);
+    split_hl(__ldg(src + (int64_t)r * sr + (int64_t)n * sn + (int64_t)ho * sh + (int64_t)wo * sw), h, l);
+  }
+  hi[(int64_t)r * kp + k] = h;
+  lo[(int64_t)r * kp + k] = l;
+}
+
+// out[i * ld + j] (a row-major matrix whose row index runs along the TMEM lanes)
+struct OutRows {
+  float* p;
+  int Mi, Nj;
+  int64_t ld;
+  struct Row {
+    float* p;
+  };
+  __device__ __forceinline__ Row row(int, int i) const {
+    Row o;
+    o.p = i < Mi ? p + (int64_t)i * ld : nullptr;
+    return o;
+  }
+  __device__ __forceinline__ void put(const Row& rw, int j, float v) const {
+    if (rw.p && j < Nj) rw.p[j] = v;
+  }
+};
+
 // strided dgrad, second half: dx[n][c][h][w] = sum over the taps (r, s) that land on the
 // stride grid of Y[(c, r, s)][(n, ho, wo)], ho = (h + ph - r) / sh; taps in (r, s) order, f64
 __global__ void __launch_bounds__(256) col2im_dgrad(const float* __restrict__ Y, float* __restrict__ dx, int N, int C,
@@ -864,6 +902,106 @@ int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* gr, const pb_
   if (rc || splits == 1) return rc;
   OutMat fin{dw, C * RS, F, (int64_t)C * RS, 0};
   fold_partials<OutMat><<<grid_for((int64_t)C * RS * F, 256), 256, 0, compute_stream()>>>(part, splits, C * RS, F, fin);
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+// 1x1 grad_weight (no padding, any stride; minml/kernels.py:231-239) as a plain TMA GEMM over
+// K = N x HO x WO: dw[f][c] = sum_k g[n, f, ho, wo] x[n, c, ho*s, wo*s].  Both operands are
+// split into K-major planes by kmajor_split_grid; the larger of C and F runs along the TMEM
+// lanes (a 64-row side would leave half of each 128-lane tile idle); split K fills the SMs and
+// the partials fold in f64 in split order.
+int pb_conv2d_grad_weight_mm(const pb_tensor* x, const pb_tensor* gr, const pb_conv* p, const pb_tensor* out) {
+  static int off = -1;  // experiment hook: PB_WG_MM=0 sends 1x1 wgrad to the other kernels
+  if (off < 0) {
+    const char* e = getenv("PB_WG_MM");
+    off = e && e[0] == '0';
+  }
+  if (!g_tma || off || !driver_ok()) return PB_ERR_UNSUPPORTED;
+  if (x->dtype != PB_F32 || gr->dtype != PB_F32 || out->dtype != PB_F32) return PB_ERR_UNSUPPORTED;
+  if (!is_contiguous(*x) || !is_contiguous(*gr) || !is_contiguous(*out)) return PB_ERR_UNSUPPORTED;
+  if (out->shape[2] != 1 || out->shape[3] != 1 || p->pad_h || p->pad_w) return PB_ERR_UNSUPPORTED;
+  const int64_t N = x->shape[0], C = x->shape[1], H = x->shape[2], W = x->shape[3], F = out->shape[0];
+  const int64_t HO = gr->shape[2], WO = gr->shape[3];
+  const int64_t K = N * HO * WO;
+  if (C < 64 || F < 64 || K < 256 || !fits(K * (C > F ? C : F)) || !fits(N * C * H * W) || !fits(N * F * HO * WO))
+    return PB_ERR_UNSUPPORTED;
+  // measured per shape (tools/conv_table.py, ResNet-50 b32): the plane pre-pass pays off for
+  // strided projections (0.246 -> 0.132 ms at 56->28) and for 14x14 / 7x7 planes; at 28x28
+  // and 56x56 stride 1 the other kernels win
+  static int force = -1;  // experiment hook: PB_WG_MM=2 takes every eligible shape
+  if (force < 0) {
+    const char* e = getenv("PB_WG_MM");
+    force = e && e[0] == '2';
+  }
+  if (!force && p->stride_h == 1 && p->stride_w == 1 && HO * WO > 196) return PB_ERR_UNSUPPORTED;
+  const bool swap = C < F;  // rows i of D: the larger channel count
+  const int64_t Mi = swap ? F : C, Nj = swap ? C : F;
+  const int BN = Nj <= 64 ? 64 : 128;
+  const int64_t kp = (K + 3) / 4 * 4;
+  Prob pr{};
+  pr.plain = 1;
+  pr.Mi = (int)Mi;
+  pr.Nj = (int)Nj;
+  pr.K = (int)kp;
+  pr.C = (int)kp;
+  pr.KH = pr.KW = pr.SH = pr.SW = 1;
+  const int64_t tiles = ((Mi + BM - 1) / BM) * ((Nj + BN - 1) / BN);
+  const int64_t kblocks = (kp + BK - 1) / BK;
+  int splits = (int)(num_sms() / tiles);
+  if (splits > kblocks / 4) splits = (int)(kblocks / 4);
+  if (splits < 1) splits = 1;
+  const int per = (int)((kblocks + splits - 1) / splits) * BK;
+  splits = (int)((kp + per - 1) / per);
+  pr.kper = per;
+  pr.zdim = splits;
+  const size_t ib = ((size_t)Mi * kp * 4 + 1023) / 1024 * 1024, jb = ((size_t)Nj * kp * 4 + 1023) / 1024 * 1024;
+  const size_t part = splits > 1 ? (size_t)splits * Mi * Nj * 4 : 0;
+  char* ws = (char*)workspace(2 * ib + 2 * jb + part);
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_weight (mm): no workspace");
+  float *ih = (float*)ws, *il = (float*)(ws + ib), *jh = (float*)(ws + 2 * ib), *jl = (float*)(ws + 2 * ib + jb);
+  float* pw = (float*)(ws + 2 * ib + 2 * jb);
+  cudaStream_t s = compute_stream();
+  const FastDiv fP((uint32_t)(HO * WO)), fWO((uint32_t)WO);
+  const float* px = (const float*)(uintptr_t)x->ptr;
+  const float* pg = (const float*)(uintptr_t)gr->ptr;
+  // x operand: rows c, k -> x[n, c, ho*sh, wo*sw]; g operand: rows f, k -> g[n, f, ho, wo]
+  const float* src_i = swap ? pg : px;
+  const float* src_j = swap ? px : pg;
+  const int64_t xs[4] = {H * W, C * H * W, (int64_t)p->stride_h * W, (int64_t)p->stride_w};
+  const int64_t gs[4] = {HO * WO, F * HO * WO, WO, 1};
+  const int64_t* si = swap ? gs : xs;
+  const int64_t* sj = swap ? xs : gs;
+  kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Mi + 7) / 8)), 256, 0, s>>>(
+      src_i, ih, il, (int)Mi, (int)K, (int)kp, si[0], si[1], si[2], si[3], fP, fWO);
+  PB_LAUNCHED();
+  kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Nj + 7) / 8)), 256, 0, s>>>(
+      src_j, jh, jl, (int)Nj, (int)K, (int)kp, sj[0], sj[1], sj[2], sj[3], fP, fWO);
+  PB_LAUNCHED();
+  CUtensorMap ah, al, bh, bl;
+  if (!map_2d(&ah, ih, kp, Mi, BM) || !map_2d(&al, il, kp, Mi, BM) || !map_2d(&bh, jh, kp, Nj, BN) ||
+      !map_2d(&bl, jl, kp, Nj, BN))
+    return fail(PB_ERR_CUDA, "wgrad (mm): tensor map encoding failed");
+  float* dw = (float*)(uintptr_t)out->ptr;
+  // dw[f][c]: rows i = c (ld 1 along i, F... ) -- OutMat puts (i, j) at i + j * ld; OutRows at i * ld + j
+  if (splits == 1) {
+    if (swap) {
+      OutRows o{dw, (int)Mi, (int)Nj, C};
+      return BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, o) : launch<128, false>(ah, al, bh, bl, pr, o);
+    }
+    OutMat o{dw, (int)Mi, (int)Nj, C, 0};
+    return BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, o) : launch<128, false>(ah, al, bh, bl, pr, o);
+  }
+  OutPartial op{pw, (int)Mi, (int)Nj};
+  int rc = BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, op) : launch<128, false>(ah, al, bh, bl, pr, op);
+  if (rc) return rc;
+  if (swap) {
+    OutRows fin{dw, (int)Mi, (int)Nj, C};
+    fold_partials<OutRows><<<grid_for(Mi * Nj, 256), 256, 0, s>>>(pw, splits, (int)Mi, (int)Nj, fin);
+  } else {
+    OutMat fin{dw, (int)Mi, (int)Nj, C, 0};
+    fold_partials<OutMat><<<grid_for(Mi * Nj, 256), 256, 0, s>>>(pw, splits, (int)Mi, (int)Nj, fin);
+  }
   PB_LAUNCHED();
   return PB_OK;
 }

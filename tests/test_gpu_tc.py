@@ -178,3 +178,20 @@ def test_tma_matmul_matches_f64_reference(gpu, m, k, n):
         got = T.matmul(tg.transpose(), ta).to_host_buffer()           # [n,m] x [m,k], M = n
         want = (g.astype(np.float64).T @ a.astype(np.float64)).astype(np.float32)
         assert rel_err(got, want) <= TOL
+
+
+@pytest.mark.parametrize("n,c,h,f,s", [(8, 64, 14, 128, 1), (4, 96, 20, 64, 2), (8, 128, 14, 256, 1), (2, 256, 28, 64, 2),
+                                       (16, 256, 7, 64, 1)])
+def test_wgrad_1x1_gemm_matches_f64_reference(gpu, n, c, h, f, s):
+    """pb_conv2d_grad_weight_mm: 1x1 grad_weight (minml/kernels.py:231-239) as a TMA GEMM over
+    K = N*HO*WO, with the larger channel count on the TMEM lanes, stride 1 and 2, against
+    the f64 sum over the gradient grid."""
+    r = np.random.default_rng(n * c + h + f + s)
+    x = r.standard_normal((n, c, h, h)).astype(np.float32)
+    ho = (h - 1) // s + 1
+    g = r.standard_normal((n, f, ho, ho)).astype(np.float32)
+    tx, tg = T.tensor(x, backend=gpu.name), T.tensor(g, backend=gpu.name)
+    got = T.conv2d_grad_weight(tx, tg, (f, c, 1, 1), s, 0).to_host_buffer()
+    xs = x[:, :, ::s, ::s].astype(np.float64)
+    want = np.einsum("nfhw,nchw->fc", g.astype(np.float64), xs).astype(np.float32)[:, :, None, None]
+    assert rel_err(got, want) <= TOL
