@@ -103,6 +103,20 @@ static bool map_im2col(CUtensorMap* m, const float* p, int N, int H, int W, int 
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// the same with explicit corners (a stride-1 walk whose first and last base positions are
+// `lower` and W - 1 + `upper`: the sub-pixel dgrad classes have asymmetric halos)
+static bool map_im2col_lu(CUtensorMap* m, const float* p, int N, int H, int W, int C, int lw, int lh, int uw, int uh,
+                          int pixels) {
+  cuuint64_t dim[4] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t str[3] = {(cuuint64_t)C * 4, (cuuint64_t)W * C * 4, (cuuint64_t)H * W * C * 4};
+  int lower[2] = {lw, lh};
+  int upper[2] = {uw, uh};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return g_im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)p, dim, str, lower, upper, 32, (cuuint32_t)pixels,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---- PTX: TMA loads, expect-tx --------------------------------------------------------------
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
@@ -577,6 +591,27 @@ struct OutRows {
   }
 };
 
+// sub-pixel dgrad weights: class (ah, aw) of a stride-s dgrad keeps the taps r = ah + p - s*d
+// (d = dh0 + tr, tr < th) and s' = aw + p - s*d' (d' = dw0 + ts, ts < tw); plane
+// [C][(tr, ts, f)] (K-major over the gradient's channels f), taps in increasing displacement
+__global__ void weight_split_class(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int F,
+                                   int Cc, int KH, int KW, int rh0, int th, int rw0, int tw, int s) {
+  const int64_t n = (int64_t)Cc * th * tw * F;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
+    const int f = (int)(idx % F);
+    int64_t t = idx / F;
+    const int ts = (int)(t % tw);
+    t /= tw;
+    const int tr = (int)(t % th);
+    const int c = (int)(t / th);
+    const int r = rh0 - s * tr, q = rw0 - s * ts;  // tap for displacement dh0 + tr, dw0 + ts
+    float h, l;
+    split_hl(w[(((int64_t)f * Cc + c) * KH + r) * KW + q], h, l);
+    hi[idx] = h;
+    lo[idx] = l;
+  }
+}
+
 // strided dgrad, second half: dx[n][c][h][w] = sum over the taps (r, s) that land on the
 // stride grid of Y[(c, r, s)][(n, ho, wo)], ho = (h + ph - r) / sh; taps in (r, s) order, f64
 __global__ void __launch_bounds__(256) col2im_dgrad(const float* __restrict__ Y, float* __restrict__ dx, int N, int C,
@@ -685,6 +720,97 @@ using namespace pb::tma;
 
 static int g_tma = 1;
 
+// strided k x k dgrad by sub-pixel decomposition: output pixel (s*a + ah, s*b + aw) only meets
+// taps r = ah + p (mod s), at gradient row a + (ah + p - r) / s.  Each of the s*s classes is a
+// stride-1 correlation of g (NHWC planes, shared) with its own sub-kernel and asymmetric halo,
+// run through the TMA implicit GEMM and scattered into dx by OutScatter; the classes partition
+// dx, so there is no memset and no zero work (the useful FLOPs exactly).
+static int dgrad_subpixel(const pb_tensor* gr, const pb_tensor* w, const pb_conv* p, const pb_tensor* out) {
+  static int off = -1;  // experiment hook: PB_DG_SUB=0 keeps the col2im / gemm_tc paths
+  if (off < 0) {
+    const char* e = getenv("PB_DG_SUB");
+    off = e && e[0] == '0';
+  }
+  if (off) return PB_ERR_UNSUPPORTED;
+  const int N = (int)out->shape[0], Cx = (int)out->shape[1], H = (int)out->shape[2], W = (int)out->shape[3];
+  const int F = (int)w->shape[0], KH = (int)w->shape[2], KW = (int)w->shape[3];
+  const int HO = (int)gr->shape[2], WO = (int)gr->shape[3];
+  const int sh = p->stride_h, sw = p->stride_w, ph = p->pad_h, pw = p->pad_w;
+  if (F % 32 || Cx % 4 || Cx < 32 || N == 0 || sh > 4 || sw > 4 || ph >= KH || pw >= KW) return PB_ERR_UNSUPPORTED;
+  const int64_t act = (int64_t)N * F * HO * WO;
+  if (!fits(act) || !fits((int64_t)N * Cx * H * W) || !fits((int64_t)Cx * F * KH * KW)) return PB_ERR_UNSUPPORTED;
+  // per class: taps, first displacement, first tap, outputs
+  struct Axis {
+    int d0, t, r0, n;
+  };
+  auto axis = [](int a, int k, int pad, int s, int in, int extent) {
+    Axis x{0, 0, 0, 0};
+    x.n = a < extent ? (extent - a + s - 1) / s : 0;
+    int dmin = 1 << 20, dmax = -(1 << 20);
+    for (int r = 0; r < k; ++r) {
+      const int num = a + pad - r;
+      if (((num % s) + s) % s) continue;
+      const int d = num >= 0 ? num / s : -((-num) / s);
+      dmin = d < dmin ? d : dmin;
+      dmax = d > dmax ? d : dmax;
+    }
+    if (dmax < dmin) return x;
+    x.d0 = dmin;
+    x.t = dmax - dmin + 1;  // displacements are consecutive
+    x.r0 = a + pad - s * dmin;
+    (void)in;
+    return x;
+  };
+  for (int ah = 0; ah < sh; ++ah)  // every class needs a tap (kernel >= stride), else decline
+    for (int aw = 0; aw < sw; ++aw)
+      if ((axis(ah, KH, ph, sh, HO, H).n && !axis(ah, KH, ph, sh, HO, H).t) ||
+          (axis(aw, KW, pw, sw, WO, W).n && !axis(aw, KW, pw, sw, WO, W).t))
+        return PB_ERR_UNSUPPORTED;
+  const size_t ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
+  const size_t wb = ((size_t)Cx * F * KH * KW * 4 + 1023) / 1024 * 1024;  // >= any class's taps
+  char* ws = (char*)workspace(2 * ab + 2 * wb * sh * sw);
+  if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (sub-pixel): no workspace");
+  float *gh = (float*)ws, *gl = (float*)(ws + ab);
+  int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
+  if (rc) return rc;
+  float* dx = (float*)(uintptr_t)out->ptr;
+  for (int ah = 0; ah < sh; ++ah) {
+    const Axis xh = axis(ah, KH, ph, sh, HO, H);
+    for (int aw = 0; aw < sw; ++aw) {
+      const Axis xw = axis(aw, KW, pw, sw, WO, W);
+      if (xh.n == 0 || xw.n == 0) continue;
+      float* whi = (float*)(ws + 2 * ab + (size_t)(2 * (ah * sw + aw)) * wb);
+      float* wlo = (float*)(ws + 2 * ab + (size_t)(2 * (ah * sw + aw) + 1) * wb);
+      weight_split_class<<<grid_for((int64_t)Cx * xh.t * xw.t * F, 256), 256, 0, compute_stream()>>>(
+          (const float*)(uintptr_t)w->ptr, whi, wlo, F, Cx, KH, KW, xh.r0, xh.t, xw.r0, xw.t, sh);
+      PB_LAUNCHED();
+      Prob pr{};
+      pr.N = N, pr.H = HO, pr.W = WO, pr.C = F;
+      pr.KH = xh.t, pr.KW = xw.t, pr.SH = 1, pr.SW = 1, pr.PH = -xh.d0, pr.PW = -xw.d0;
+      pr.HO = xh.n, pr.WO = xw.n;
+      pr.fP = FastDiv((uint32_t)(xh.n * xw.n));
+      pr.fWO = FastDiv((uint32_t)xw.n);
+      pr.F = Cx;
+      pr.Mi = N * xh.n * xw.n;
+      pr.Nj = Cx;
+      pr.K = F * xh.t * xw.t;
+      pr.zdim = 1;
+      if (!fits((int64_t)pr.Mi * Cx)) return PB_ERR_UNSUPPORTED;
+      const int BN = Cx <= 64 ? 64 : 128;
+      CUtensorMap am, al, bm, bl;
+      const int uw = xw.n + xw.d0 - WO, uh = xh.n + xh.d0 - HO;
+      if (!map_im2col_lu(&am, gh, N, HO, WO, F, xw.d0, xh.d0, uw, uh, BM) ||
+          !map_im2col_lu(&al, gl, N, HO, WO, F, xw.d0, xh.d0, uw, uh, BM) ||
+          !map_2d(&bm, whi, pr.K, Cx, BN) || !map_2d(&bl, wlo, pr.K, Cx, BN))
+        return fail(PB_ERR_CUDA, "dgrad (sub-pixel): tensor map encoding failed");
+      OutScatter o{dx + (int64_t)ah * W + aw, pr.Mi, Cx, pr.fP, pr.fWO, sh, sw, W, H * W};
+      rc = BN == 64 ? launch<64, false>(am, al, bm, bl, pr, o) : launch<128, false>(am, al, bm, bl, pr, o);
+      if (rc) return rc;
+    }
+  }
+  return PB_OK;
+}
+
 extern "C" {
 
 int pb_tma_enable(int on) {
@@ -757,6 +883,10 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
     OutScatter o{(float*)(uintptr_t)out->ptr, (int)rows, Cx, FastDiv((uint32_t)(HO * WO)), FastDiv((uint32_t)WO),
                  p->stride_h, p->stride_w, W, H * W};
     return run_conv(pr, gh, gl, wh, wl, o);
+  }
+  if ((p->stride_h > 1 || p->stride_w > 1) && KH > 1) {
+    int rc = dgrad_subpixel(gr, w, p, out);
+    if (rc != PB_ERR_UNSUPPORTED) return rc;
   }
   if ((p->stride_h != 1 || p->stride_w != 1) && ((int64_t)N * HO * WO <= 8192 || Cx < 16)) {
     // strided k x k: Y = W^T g as a GEMM over the gradient pixels (rows) and the (c, r, s)

@@ -396,6 +396,65 @@ __global__ void __launch_bounds__(256) red_cols4_sum(RedArgs r) {
   }
 }
 
+// the same walk for fewer outputs: a block owns 128 consecutive outputs (32 lanes x float4)
+// and its 8 warps take consecutive slices of the reduced axis; the slice sums fold in slice
+// order through shared memory (the [1, C, H, W] sum(2) and [N, C] sum(0) of _unbroadcast)
+__global__ void __launch_bounds__(256) red_cols4s_sum(RedArgs r) {
+  __shared__ double part[8][32][4];
+  const float* a = (const float*)r.a;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const int64_t R = r.R, sR = r.sR, slice = (R + 7) / 8;
+  const int64_t j0 = wp * slice, j1 = j0 + slice < R ? j0 + slice : R;
+  for (int64_t o0 = (int64_t)blockIdx.x * 128; o0 < r.O; o0 += (int64_t)gridDim.x * 128) {
+    const int64_t o = o0 + lane * 4;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    if (o < r.O) {
+      const float* p = a + out_base(r, o);
+      int64_t j = j0;
+      for (; j + 4 <= j1; j += 4) {
+        float4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(p + (j + u) * sR));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          s0 += (double)v[u].x;
+          s1 += (double)v[u].y;
+          s2 += (double)v[u].z;
+          s3 += (double)v[u].w;
+        }
+      }
+      for (; j < j1; ++j) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p + j * sR));
+        s0 += (double)v.x;
+        s1 += (double)v.y;
+        s2 += (double)v.z;
+        s3 += (double)v.w;
+      }
+    }
+    part[wp][lane][0] = s0;
+    part[wp][lane][1] = s1;
+    part[wp][lane][2] = s2;
+    part[wp][lane][3] = s3;
+    __syncthreads();
+    if (wp == 0 && o < r.O) {
+#pragma unroll
+      for (int t = 1; t < 8; ++t) {
+        s0 += part[t][lane][0];
+        s1 += part[t][lane][1];
+        s2 += part[t][lane][2];
+        s3 += part[t][lane][3];
+      }
+      typedef Red<PB_SUM, float>::Acc Acc;
+      Acc c0{s0, -1}, c1{s1, -1}, c2{s2, -1}, c3{s3, -1};
+      emit<PB_SUM, float>(r, o, 0, c0);
+      emit<PB_SUM, float>(r, o + 1, 0, c1);
+      emit<PB_SUM, float>(r, o + 2, 0, c2);
+      emit<PB_SUM, float>(r, o + 3, 0, c3);
+    }
+    __syncthreads();
+  }
+}
+
 // fold chunk partials in chunk order
 template <int OP, typename T>
 __global__ void __launch_bounds__(256) red_final(RedArgs r) {
@@ -497,9 +556,15 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int ep
       r.chunk = r.R;
       r.partial = nullptr;
       const int64_t threads = r.O / 4;
-      const int64_t blocks = (threads + 255) / 256;
-      const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
-      red_cols4_sum<<<grid, 256, 0, s>>>(r);
+      if (threads >= (int64_t)num_sms() * 512 || r.R < 16) {  // enough outputs: one thread walks all of R
+        const int64_t blocks = (threads + 255) / 256;
+        const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+        red_cols4_sum<<<grid, 256, 0, s>>>(r);
+      } else {  // few outputs: 8 warps split R
+        const int64_t blocks = (r.O + 127) / 128;
+        const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
+        red_cols4s_sum<<<grid, 256, 0, s>>>(r);
+      }
       PB_LAUNCHED();
       return PB_OK;
     }

@@ -195,3 +195,31 @@ def test_wgrad_1x1_gemm_matches_f64_reference(gpu, n, c, h, f, s):
     xs = x[:, :, ::s, ::s].astype(np.float64)
     want = np.einsum("nfhw,nchw->fc", g.astype(np.float64), xs).astype(np.float32)[:, :, None, None]
     assert rel_err(got, want) <= TOL
+
+
+def _np_dgrad(g, w, xshape, s, p):
+    """f64 adjoint of the strided cross-correlation: scatter every tap's contribution."""
+    n, c, h, wd = xshape
+    _, _, kh, kw = w.shape
+    ho, wo = g.shape[2], g.shape[3]
+    dx = np.zeros((n, c, h + 2 * p + s, wd + 2 * p + s))
+    g64, w64 = g.astype(np.float64), w.astype(np.float64)
+    for r in range(kh):
+        for q in range(kw):
+            dx[:, :, r:r + s * ho:s, q:q + s * wo:s] += np.einsum("nfhw,fc->nchw", g64, w64[:, :, r, q])
+    return dx[:, :, p:p + h, p:p + wd].astype(np.float32)
+
+
+@pytest.mark.parametrize("n,c,h,f,k,s,p", [(4, 64, 16, 64, 3, 2, 1), (2, 128, 15, 96, 3, 2, 1), (2, 32, 14, 64, 5, 2, 2),
+                                           (2, 64, 13, 32, 3, 3, 1), (3, 96, 12, 128, 4, 2, 1)])
+def test_subpixel_dgrad_matches_f64_reference(gpu, n, c, h, f, k, s, p):
+    """Strided k x k grad_input by sub-pixel decomposition (one stride-1 TMA implicit GEMM per
+    output phase class, asymmetric halos, scattered into dx; minml/kernels.py:213-228)
+    against the f64 adjoint, including odd extents, k = 4 and 5, and stride 3."""
+    r = np.random.default_rng(n + c + h + f + k + s)
+    ho = (h + 2 * p - k) // s + 1
+    g = r.standard_normal((n, f, ho, ho)).astype(np.float32)
+    w = (r.standard_normal((f, c, k, k)) / np.sqrt(f * k * k)).astype(np.float32)
+    got = T.conv2d_grad_input(T.tensor(g, backend=gpu.name), T.tensor(w, backend=gpu.name), (n, c, h, h), s,
+                              p).to_host_buffer()
+    assert rel_err(got, _np_dgrad(g, w, (n, c, h, h), s, p)) <= TOL
