@@ -573,6 +573,28 @@ __global__ void __launch_bounds__(256) kmajor_split_grid(const float* __restrict
   lo[(int64_t)r * kp + k] = l;
 }
 
+// kmajor_split_grid for stride-1 rows whose plane length HO*WO is a multiple of 4: each
+// thread converts 4 consecutive k (one image, contiguous in the source) with 16-byte accesses
+__global__ void __launch_bounds__(256) kmajor_split_grid4(const float* __restrict__ src, float* __restrict__ hi,
+                                                          float* __restrict__ lo, int R, int K, int kp, int64_t sr,
+                                                          int64_t sn, FastDiv fP) {
+  const int r = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int k = (blockIdx.x * 32 + (threadIdx.x & 31)) * 4;
+  if (r >= R || k >= kp) return;
+  float4 h = make_float4(0.f, 0.f, 0.f, 0.f), l = h;
+  if (k < K) {  // K % 4 == 0 here, so the vector is all in range
+    uint32_t n, q;
+    fP.divmod((uint32_t)k, n, q);
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src + (int64_t)r * sr + (int64_t)n * sn + q));
+    split_hl(v.x, h.x, l.x);
+    split_hl(v.y, h.y, l.y);
+    split_hl(v.z, h.z, l.z);
+    split_hl(v.w, h.w, l.w);
+  }
+  *reinterpret_cast<float4*>(hi + (int64_t)r * kp + k) = h;
+  *reinterpret_cast<float4*>(lo + (int64_t)r * kp + k) = l;
+}
+
 // out[i * ld + j] (a row-major matrix whose row index runs along the TMEM lanes)
 struct OutRows {
   float* p;
@@ -1056,15 +1078,17 @@ int pb_conv2d_grad_weight_mm(const pb_tensor* x, const pb_tensor* gr, const pb_c
   const int64_t K = N * HO * WO;
   if (C < 64 || F < 64 || K < 256 || !fits(K * (C > F ? C : F)) || !fits(N * C * H * W) || !fits(N * F * HO * WO))
     return PB_ERR_UNSUPPORTED;
-  // measured per shape (tools/conv_table.py, ResNet-50 b32): the plane pre-pass pays off for
-  // strided projections (0.246 -> 0.132 ms at 56->28) and for 14x14 / 7x7 planes; at 28x28
-  // and 56x56 stride 1 the other kernels win
+  // measured per shape (tools/conv_table.py, ResNet-50 b32, vectorised pre-pass): this path
+  // wins for strided projections (0.246 -> 0.132 ms at 56->28), 14x14 / 7x7 planes, and
+  // stride-1 planes with C*F >= 32768 or F > C (64->256 @56: 0.162 -> 0.123 ms); the
+  // SIMT-fed kernel keeps 64->64 and 256->64 @56x56
   static int force = -1;  // experiment hook: PB_WG_MM=2 takes every eligible shape
   if (force < 0) {
     const char* e = getenv("PB_WG_MM");
     force = e && e[0] == '2';
   }
-  if (!force && p->stride_h == 1 && p->stride_w == 1 && HO * WO > 196) return PB_ERR_UNSUPPORTED;
+  if (!force && p->stride_h == 1 && p->stride_w == 1 && HO * WO > 196 && C * F < 32768 && F <= C)
+    return PB_ERR_UNSUPPORTED;
   const bool swap = C < F;  // rows i of D: the larger channel count
   const int64_t Mi = swap ? F : C, Nj = swap ? C : F;
   const int BN = Nj <= 64 ? 64 : 128;
@@ -1102,12 +1126,22 @@ int pb_conv2d_grad_weight_mm(const pb_tensor* x, const pb_tensor* gr, const pb_c
   const int64_t gs[4] = {HO * WO, F * HO * WO, WO, 1};
   const int64_t* si = swap ? gs : xs;
   const int64_t* sj = swap ? xs : gs;
-  kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Mi + 7) / 8)), 256, 0, s>>>(
-      src_i, ih, il, (int)Mi, (int)K, (int)kp, si[0], si[1], si[2], si[3], fP, fWO);
-  PB_LAUNCHED();
-  kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Nj + 7) / 8)), 256, 0, s>>>(
-      src_j, jh, jl, (int)Nj, (int)K, (int)kp, sj[0], sj[1], sj[2], sj[3], fP, fWO);
-  PB_LAUNCHED();
+  const bool vec = p->stride_h == 1 && p->stride_w == 1 && (HO * WO) % 4 == 0 && x->ptr % 16 == 0 && gr->ptr % 16 == 0;
+  if (vec) {  // K = N*HO*WO is then a multiple of 4 too (kp == K)
+    kmajor_split_grid4<<<dim3((unsigned)((kp / 4 + 31) / 32), (unsigned)((Mi + 7) / 8)), 256, 0, s>>>(
+        src_i, ih, il, (int)Mi, (int)K, (int)kp, si[0], si[1], fP);
+    PB_LAUNCHED();
+    kmajor_split_grid4<<<dim3((unsigned)((kp / 4 + 31) / 32), (unsigned)((Nj + 7) / 8)), 256, 0, s>>>(
+        src_j, jh, jl, (int)Nj, (int)K, (int)kp, sj[0], sj[1], fP);
+    PB_LAUNCHED();
+  } else {
+    kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Mi + 7) / 8)), 256, 0, s>>>(
+        src_i, ih, il, (int)Mi, (int)K, (int)kp, si[0], si[1], si[2], si[3], fP, fWO);
+    PB_LAUNCHED();
+    kmajor_split_grid<<<dim3((unsigned)((kp + 31) / 32), (unsigned)((Nj + 7) / 8)), 256, 0, s>>>(
+        src_j, jh, jl, (int)Nj, (int)K, (int)kp, sj[0], sj[1], sj[2], sj[3], fP, fWO);
+    PB_LAUNCHED();
+  }
   CUtensorMap ah, al, bh, bl;
   if (!map_2d(&ah, ih, kp, Mi, BM) || !map_2d(&al, il, kp, Mi, BM) || !map_2d(&bh, jh, kp, Nj, BN) ||
       !map_2d(&bl, jl, kp, Nj, BN))
