@@ -628,12 +628,12 @@ __global__ void __launch_bounds__(Cfg<BN>::THREADS, 1)
 // weight re-layout: dst[a][(r*KW+s)*Bn + bb] = w[f][c][r][s] with (a,bb) = (f,c) (fprop,
 // k = (r,s,c)) or (c,f) (dgrad, k = (r,s,f))
 __global__ void weight_rsk(const float* w, float* dst, int F, int Cc, int RS, int dgrad) {
-  int64_t n = (int64_t)F * Cc * RS;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    int rs = (int)(idx % RS);
-    int64_t t = idx / RS;
-    int c = (int)(t % Cc);
-    int f = (int)(t / Cc);
+  const uint32_t n = (uint32_t)F * Cc * RS;  // weights: far below 2^31 elements (checked on the host)
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    int rs = (int)(idx % (uint32_t)RS);
+    uint32_t t = idx / (uint32_t)RS;
+    int c = (int)(t % (uint32_t)Cc);
+    int f = (int)(t / (uint32_t)Cc);
     float v = w[idx];
     if (!dgrad)
       dst[((int64_t)f * RS + rs) * Cc + c] = v;
@@ -797,6 +797,7 @@ int pb_conv2d_tc(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias, 
   int64_t rows = (int64_t)g.N * g.HO * g.WO, K = (int64_t)g.C * g.KH * g.KW;
   if (rows == 0 || g.F == 0 || K == 0) return PB_ERR_UNSUPPORTED;
   if (!fits_i32(rows * g.F) || !fits_i32((int64_t)g.N * g.C * g.H * g.W)) return PB_ERR_UNSUPPORTED;
+  if (!fits_i32((int64_t)g.F * K)) return PB_ERR_UNSUPPORTED;  // weight_rsk indexes in 32 bits
   size_t wbytes = ((size_t)g.F * K * 4 + 255) / 256 * 256;
   char* ws = (char*)workspace(wbytes + split_ws_bytes((int)rows, g.F));
   if (!ws) return fail(PB_ERR_OOM, "conv2d: no workspace");
@@ -830,6 +831,7 @@ int pb_conv2d_grad_input_tc(const pb_tensor* gr, const pb_tensor* w, const pb_co
   int64_t rows = (int64_t)g.N * g.H * g.W, K = (int64_t)g.F * g.KH * g.KW;
   if (rows == 0 || g.C == 0 || K == 0 || g.F % 4 != 0) return PB_ERR_UNSUPPORTED;  // wt rows 16B-aligned
   if (!fits_i32(rows * g.C) || !fits_i32((int64_t)g.N * g.F * g.HO * g.WO)) return PB_ERR_UNSUPPORTED;
+  if (!fits_i32((int64_t)g.C * K)) return PB_ERR_UNSUPPORTED;  // weight_rsk indexes in 32 bits
   size_t wbytes = ((size_t)g.C * K * 4 + 255) / 256 * 256;
   char* ws = (char*)workspace(wbytes + split_ws_bytes((int)rows, g.C));
   if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input: no workspace");

@@ -499,13 +499,14 @@ __global__ void __launch_bounds__(256) split_planes(const float* __restrict__ x,
 // weights w[f][c][r][s] -> hi/lo[a][(r,s,b)]: fprop (a,b) = (f,c); dgrad (a,b) = (c,f) with the
 // taps flipped (r,s) -> (KH-1-r, KW-1-s)
 __global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int F,
-                             int Cc, int KH, int KW, int dgrad) {
+                             int Cc, int KH, int KW, int dgrad, FastDiv fRS, FastDiv fC) {
   const int RS = KH * KW;
-  const int64_t n = (int64_t)F * Cc * RS;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int rs = (int)(idx % RS);
-    const int64_t t = idx / RS;
-    const int c = (int)(t % Cc), f = (int)(t / Cc);
+  const uint32_t n = (uint32_t)F * Cc * RS;  // < 2^31 (the callers' fits() checks)
+  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
+    uint32_t t, rsu, fu, cu;
+    fRS.divmod(idx, t, rsu);
+    fC.divmod(t, fu, cu);
+    const int rs = (int)rsu, c = (int)cu, f = (int)fu;
     float h, l;
     split_hl(w[idx], h, l);
     int64_t d;
@@ -864,8 +865,7 @@ int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias,
   char* ws = (char*)workspace(2 * wb + 2 * ab);
   if (!ws) return fail(PB_ERR_OOM, "conv2d (tma): no workspace");
   float *wh = (float*)ws, *wl = (float*)(ws + wb), *xh = (float*)(ws + 2 * wb), *xl = (float*)(ws + 2 * wb + ab);
-  weight_split<<<grid_for((int64_t)F * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F,
-                                                                            C, KH, KW, 0);
+  weight_split<<<grid_for((int64_t)F * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, C, KH, KW, 0, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(C)));
   PB_LAUNCHED();
   int rc = split_act((const float*)(uintptr_t)x->ptr, xh, xl, N, C, H * W);
   if (rc) return rc;
@@ -897,8 +897,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
     if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
     float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
     PB_CUDA(cudaMemsetAsync((void*)(uintptr_t)out->ptr, 0, (size_t)N * Cx * H * W * 4, compute_stream()));
-    weight_split<<<grid_for((int64_t)Cx * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl,
-                                                                               F, Cx, 1, 1, 1);
+    weight_split<<<grid_for((int64_t)Cx * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, 1, 1, 1, FastDiv((uint32_t)((1) * (1))), FastDiv((uint32_t)(Cx)));
     PB_LAUNCHED();
     int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
     if (rc) return rc;
@@ -932,8 +931,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
     if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
     float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
     float* Y = (float*)(ws + 2 * wb + 2 * ab);
-    weight_split<<<grid_for(cols * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx,
-                                                                        KH, KW, 2);
+    weight_split<<<grid_for(cols * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 2, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(Cx)));
     PB_LAUNCHED();
     int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
     if (rc) return rc;
@@ -961,8 +959,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
   char* ws = (char*)workspace(2 * wb + 2 * ab);
   if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
   float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
-  weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl,
-                                                                             F, Cx, KH, KW, 1);
+  weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 1, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(Cx)));
   PB_LAUNCHED();
   int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
   if (rc) return rc;
