@@ -500,27 +500,27 @@ __global__ void __launch_bounds__(256) split_planes(const float* __restrict__ x,
 // taps flipped (r,s) -> (KH-1-r, KW-1-s)
 __global__ void weight_split(const float* __restrict__ w, float* __restrict__ hi, float* __restrict__ lo, int F,
                              int Cc, int KH, int KW, int dgrad, FastDiv fRS, FastDiv fC) {
+  // walks the OUTPUT index so the two planes are written coalesced; the (small, L2-resident)
+  // weights are gathered.  fC divides by the plane's innermost extent: Cc (fprop) or F (dgrad)
   const int RS = KH * KW;
   const uint32_t n = (uint32_t)F * Cc * RS;  // < 2^31 (the callers' fits() checks)
-  for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    uint32_t t, rsu, fu, cu;
-    fRS.divmod(idx, t, rsu);
-    fC.divmod(t, fu, cu);
-    const int rs = (int)rsu, c = (int)cu, f = (int)fu;
-    float h, l;
-    split_hl(w[idx], h, l);
-    int64_t d;
-    if (dgrad == 2) {  // columns of the strided dgrad GEMM: [(c, r, s)][f]
-      d = ((int64_t)c * RS + rs) * F + f;
-    } else if (!dgrad) {
-      d = ((int64_t)f * RS + rs) * Cc + c;
-    } else {
-      const int r = rs / KW, s = rs - r * KW;
-      const int fr = (KH - 1 - r) * KW + (KW - 1 - s);
-      d = ((int64_t)c * RS + fr) * F + f;
+  for (uint32_t o = blockIdx.x * blockDim.x + threadIdx.x; o < n; o += gridDim.x * blockDim.x) {
+    uint32_t t, inner, outer, rsu;
+    fC.divmod(o, t, inner);
+    fRS.divmod(t, outer, rsu);
+    int f, c, rs = (int)rsu;
+    if (!dgrad) {  // o = (f*RS + rs)*Cc + c
+      f = (int)outer;
+      c = (int)inner;
+    } else {       // o = (c*RS + rs')*F + f; dgrad == 1 stores the taps flipped: rs' = RS-1-rs
+      f = (int)inner;
+      c = (int)outer;
+      if (dgrad == 1) rs = RS - 1 - rs;
     }
-    hi[d] = h;
-    lo[d] = l;
+    float h, l;
+    split_hl(__ldg(w + ((int64_t)f * Cc + c) * RS + rs), h, l);
+    hi[o] = h;
+    lo[o] = l;
   }
 }
 
@@ -897,7 +897,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
     if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
     float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
     PB_CUDA(cudaMemsetAsync((void*)(uintptr_t)out->ptr, 0, (size_t)N * Cx * H * W * 4, compute_stream()));
-    weight_split<<<grid_for((int64_t)Cx * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, 1, 1, 1, FastDiv((uint32_t)((1) * (1))), FastDiv((uint32_t)(Cx)));
+    weight_split<<<grid_for((int64_t)Cx * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, 1, 1, 1, FastDiv((uint32_t)((1) * (1))), FastDiv((uint32_t)(F)));
     PB_LAUNCHED();
     int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
     if (rc) return rc;
@@ -931,7 +931,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
     if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
     float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
     float* Y = (float*)(ws + 2 * wb + 2 * ab);
-    weight_split<<<grid_for(cols * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 2, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(Cx)));
+    weight_split<<<grid_for(cols * F, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 2, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(F)));
     PB_LAUNCHED();
     int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
     if (rc) return rc;
@@ -959,7 +959,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
   char* ws = (char*)workspace(2 * wb + 2 * ab);
   if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
   float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
-  weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 1, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(Cx)));
+  weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 1, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(F)));
   PB_LAUNCHED();
   int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
   if (rc) return rc;
