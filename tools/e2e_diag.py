@@ -1,5 +1,5 @@
-"""Where does the e2e step lose time against graph-only replay?  Times ResNet-50 b32
-CapturedStep variants with wall clock + CUDA events (diagnostic only)."""
+"""Where does the pipelined e2e step (CapturedStep.run) lose time against graph-only replay?
+ResNet-50 b32, page-locked batch; CUDA events + wall clock per variant (diagnostic only)."""
 import os
 import sys
 import time
@@ -15,37 +15,46 @@ be.seed(0)
 model = models.resnet50(backend=be.name)
 opt = optim.SGD(model.params(), lr=0.01, momentum=0.9)
 r = np.random.default_rng(0)
-x = r.standard_normal((32, 3, 224, 224)).astype(np.float32)
-y = r.integers(0, 1000, 32).astype(np.int64)
+x = be.pinned((32, 3, 224, 224), np.float32)
+x[...] = r.standard_normal((32, 3, 224, 224)).astype(np.float32)
+y = be.pinned((32,), np.int64)
+y[...] = r.integers(0, 1000, 32)
 step = training.CapturedStep(model, opt, warmup=2)
 for _ in range(4):
     step(x, y)
+list(step.run([(x, y)] * 2))
 be.synchronize()
-K = 10
+K = 20
 
 
 def timed(name, fn):
     be.synchronize()
     t0 = time.perf_counter()
     stop = be.event_timer()
-    for _ in range(K):
-        fn()
+    fn()
     ms = stop() / K
-    print(f"{name:40s} events {ms:7.3f} ms  wall {(time.perf_counter() - t0) * 1e3 / K:7.3f} ms", flush=True)
+    print(f"{name:44s} events {ms:7.3f} ms  wall {(time.perf_counter() - t0) * 1e3 / K:7.3f} ms", flush=True)
 
 
-timed("graph only", lambda: step.graph.launch())
-timed("copy_in x,y (compute stream)", lambda: (be.copy_in(step.x, x), be.copy_in(step.y, y)))
-timed("graph + copy_in", lambda: (be.copy_in(step.x, x), be.copy_in(step.y, y), step.graph.launch()))
-timed("graph + loss.scalar", lambda: (step.graph.launch(), step.loss.scalar()))
-timed("step(x, y)", lambda: step(x, y))
-sx = be  # noqa
-t0 = time.perf_counter()
-for _ in range(K):
-    np.ascontiguousarray(x).copy()
-print(f"host copy of x: {(time.perf_counter() - t0) * 1e3 / K:.3f} ms")
-be.synchronize()
-t0 = time.perf_counter()
-stop = be.event_timer()
-n = len(list(step.run([(x, y)] * K)))
-print(f"run() x{n}: events {stop() / K:.3f} ms wall {(time.perf_counter() - t0) * 1e3 / K:.3f} ms")
+timed("graph only", lambda: [step.graph.launch() for _ in range(K)])
+timed("step(x, y) (sync per step)", lambda: [step(x, y) for _ in range(K)])
+timed("run() pipelined", lambda: list(step.run([(x, y)] * K)))
+
+
+def h2d_only():
+    for _ in range(K):
+        be.stage_in(step.x, x, stream=2)
+        be.stream_sync(2)
+
+
+timed("stage_in x on copy stream + sync", h2d_only)
+
+
+def graph_plus_copystream():
+    for _ in range(K):
+        be.stage_in(step._stage[0][0], x, stream=2)
+        step.graph.launch()
+    be.stream_sync(2)
+
+
+timed("graph + concurrent copy-stream H2D", graph_plus_copystream)
