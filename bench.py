@@ -13,8 +13,9 @@ Prints ONE JSON line on rank 0.
 * ``e2e``    the same through the public API ``training.train_step`` with host numpy
   batches: every step copies images+labels host->device and reads the loss back.
 * ``roofline`` the dominant kernel class timed live here with CUDA events.
-* ``cpu_baseline`` the CPU oracle port of the reference on this host (bounded sample).
+* ``cpu_baseline`` the reference itself (minml, baseline/_ref) on this host's cores (bounded sample).
 ``--impl reference`` times only that CPU path (rank 0) and prints its own line.
+``--gpus N`` outside torchrun starts N ranks itself (torch.distributed.run, 127.0.0.1).
 """
 
 import argparse
@@ -35,7 +36,7 @@ METRIC = "train samples/sec + ms/iter (ResNet-50 synth) at 1/2/4/8 B200 vs CPU r
 UNIT = "samples/s"
 BATCH = 32
 CLASSES = 1000
-REF_SAMPLE_BATCH = 2  # CPU reference arm: bounded sample of the same workload
+REF_SAMPLE_BATCH = 4  # CPU reference arm: bounded sample of the same workload (a b32 step takes ~45 s)
 
 
 def peaks():
@@ -102,57 +103,182 @@ def synthetic_batch(rank, batch):
     return x, y
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _reference_modules():
+    """The UNMODIFIED reference (minml, installed into baseline/_ref by __graft_entry__.build
+    from /root/reference) plus this repo's ResNet-50 composition (models.py, which composes
+    only the namespace it is given) loaded standalone -- so the reference arm never imports
+    this package and never maps libpaper_b200.so."""
+    import importlib.util
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "minml")):
+        raise RuntimeError("baseline/_ref/minml missing (run __graft_entry__.build() in the build container)")
+    sys.path.insert(0, ref)
+    import minml
+    import minml.eager  # noqa: F401
+    import minml.models  # noqa: F401
+    import minml.training  # noqa: F401
+    spec = importlib.util.spec_from_file_location("pb_models_standalone",
+                                                  os.path.join(ROOT, "paper_2201_12465_b200", "models.py"))
+    models = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(models)
+    return minml, models
+
+
 def cpu_reference(steps, warmup, batch=REF_SAMPLE_BATCH):
-    """The reference algorithm on host cores: the numpy oracle port (oracle/) through the same
-    front end, ResNet-50 at a bounded batch.  Returns samples/s and the sample description."""
-    sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from oracle.backend import OracleBackend
-    from paper_2201_12465_b200 import models, optim, registry, training
-    be = OracleBackend(name="cpu-reference", seed=0)
-    registry.register(be)
-    model = models.resnet50(backend=be.name)
-    opt = optim.SGD(model.params(), lr=0.01, momentum=0.9)
-    x, y = synthetic_batch(0, batch)
-    for _ in range(warmup):
-        training.train_step(model, x, y, opt)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        training.train_step(model, x, y, opt)
-    dt = time.perf_counter() - t0
-    registry.unregister(be.name)
+    """The reference's own CPU implementation of the step: minml's EagerBackend (numpy +
+    OpenBLAS on every host core) running minml.training.train_step on ResNet-50 at a bounded
+    batch.  Returns (samples/s, ms/step)."""
+    minml, models = _reference_modules()
+    be = minml.eager.EagerBackend(name="cpu-reference", seed=0)
+    minml.registry.register(be)
+    try:
+        ns = models.namespace(minml.nn, minml.ops, minml._tensor, minml.autograd)
+        model = models.resnet50(backend=be.name, ns=ns)
+        opt = minml.optim.SGD(model.params(), lr=0.01, momentum=0.9)
+        x, y = synthetic_batch(0, batch)
+        for _ in range(warmup):
+            minml.training.train_step(model, x, y, opt)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            minml.training.train_step(model, x, y, opt)
+        dt = time.perf_counter() - t0
+    finally:
+        minml.registry.unregister(be.name)
     return batch * steps / dt, dt / steps * 1e3
 
 
-def kernel_roofline(be, T, hbm_peak, tc_peak):
-    """Time the dominant kernel classes of the step in isolation (CUDA events)."""
-    rng = np.random.default_rng(5)
+def cpu_overheads(n=2000):
+    """Per-op framework overhead of the reference on this host: a [1]-element
+    add through minml's eager backend, and through a no-op backend (the front-end floor)."""
+    minml, _ = _reference_modules()
+    eager = minml.eager.EagerBackend(name="cpu-overhead", seed=0)
+
+    class Null(minml.registry.Backend):
+        def execute(self, call, args):
+            return np.zeros(tuple(call.shape), call.dtype.np) if call.name == "to_host" else self
+
+    null = Null("cpu-null")
     out = {}
-    # (1) HBM-bound: BatchNorm's broadcast subtract on the largest activation
+    for key, be in (("eager_add_us", eager), ("front_end_floor_us", null)):
+        minml.registry.register(be)
+        try:
+            a = minml.tensor(np.ones(1, np.float32), backend=be.name)
+            for _ in range(100):
+                a + a
+            t0 = time.perf_counter()
+            for _ in range(n):
+                a + a
+            out[key] = (time.perf_counter() - t0) / n * 1e6
+        finally:
+            minml.registry.unregister(be.name)
+    return out
+
+
+def resnet50_convs(n):
+    """[(count, (N,C,H,W), (F,C,k,k), stride, pad)] for every conv of ResNet-50 v1.5."""
+    out = {}
+
+    def add(xs, ws, st, p):
+        out[(xs, ws, st, p)] = out.get((xs, ws, st, p), 0) + 1
+
+    add((n, 3, 224, 224), (64, 3, 7, 7), 2, 3)
+    cin, h = 64, 56
+    for stage, blocks in enumerate((3, 4, 6, 3)):
+        w = 64 * 2 ** stage
+        for i in range(blocks):
+            st = 2 if (i == 0 and stage > 0) else 1
+            add((n, cin, h, h), (w, cin, 1, 1), 1, 0)
+            add((n, w, h, h), (w, w, 3, 3), st, 1)
+            ho = (h + 2 - 3) // st + 1
+            add((n, w, ho, ho), (4 * w, w, 1, 1), 1, 0)
+            if i == 0:
+                add((n, cin, h, h), (4 * w, cin, 1, 1), st, 0)
+            cin, h = 4 * w, ho
+    return [(c,) + k for k, c in out.items()]
+
+
+def kernel_roofline(be, T, hbm_peak, tc_peak):
+    """Live CUDA-event timing of the step's dominant kernel class -- the conv2d family
+    (fprop + dgrad + wgrad of all 53 ResNet-50 convs, hi/lo pre-passes included, 785 GFLOP
+    per step) -- plus the HBM-bound broadcast subtract beside it."""
+    rng = np.random.default_rng(5)
+    total_ms, total_flops, per = 0.0, 0.0, {"fprop": 0.0, "dgrad": 0.0, "wgrad": 0.0}
+    launches = 0
+    for cnt, xs, ws, st, p in resnet50_convs(BATCH):
+        x = T.tensor(rng.standard_normal(xs).astype(np.float32), backend=be.name)
+        w = T.tensor((rng.standard_normal(ws) * 0.05).astype(np.float32), backend=be.name)
+        y = T.conv2d(x, w, None, st, p)
+        g = T.tensor(rng.standard_normal(tuple(y.shape)).astype(np.float32), backend=be.name)
+        flops = 2.0 * xs[0] * ws[0] * y.shape[2] * y.shape[3] * ws[1] * ws[2] * ws[3]
+        ops = {"fprop": lambda: T.conv2d(x, w, None, st, p),
+               "dgrad": lambda: T.conv2d_grad_input(g, w, xs, st, p),
+               "wgrad": lambda: T.conv2d_grad_weight(x, g, ws, st, p)}
+        for name, fn in ops.items():
+            fn()
+            l0 = be.launch_count()
+            stop = be.event_timer()
+            for _ in range(3):
+                fn()
+            ms = stop() / 3
+            launches += cnt * (be.launch_count() - l0) // 3
+            per[name] += cnt * ms
+            total_ms += cnt * ms
+            total_flops += cnt * flops
+    out = {"conv": {"bound": "tensor", "achieved": total_flops / total_ms / 1e9, "peak": tc_peak, "unit": "TFLOP/s",
+                    "kernel": "conv2d family: fprop+dgrad+wgrad of the 53 ResNet-50 b32 convs (tcgen05 3xTF32, "
+                              "incl. hi/lo pre-passes)", "ms_per_step": total_ms, "gflop_per_step": total_flops / 1e9,
+                    "ms_by_kind": per, "launches_per_step": launches}}
+    # HBM-bound: BatchNorm's broadcast subtract on the largest activation
     x = T.tensor(rng.standard_normal((32, 256, 56, 56)).astype(np.float32), backend=be.name)
     m = T.tensor(rng.standard_normal((1, 256, 1, 1)).astype(np.float32), backend=be.name)
     for _ in range(3):
         x - m
-    reps = 20
     stop = be.event_timer()
-    for _ in range(reps):
+    for _ in range(20):
         x - m
-    ms = stop() / reps
+    ms = stop() / 20
     nbytes = 2 * x.shape.size * 4 + 256 * 4
     out["ew"] = {"bound": "hbm", "achieved": nbytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
                  "kernel": "ew broadcast sub f32 [32,256,56,56]-[1,256,1,1]", "ms": ms}
-    # (2) tensor-bound: 3x3 conv fprop, ResNet stage-1 shape
-    xs, ws = (32, 64, 56, 56), (64, 64, 3, 3)
-    xc = T.tensor(rng.standard_normal(xs).astype(np.float32), backend=be.name)
-    wc = T.tensor((rng.standard_normal(ws) * 0.05).astype(np.float32), backend=be.name)
-    T.conv2d(xc, wc, None, 1, 1)
-    stop = be.event_timer()
-    for _ in range(5):
-        T.conv2d(xc, wc, None, 1, 1)
-    ms = stop() / 5
-    flops = 2 * 32 * 64 * 56 * 56 * 64 * 9
-    out["conv"] = {"bound": "tensor", "achieved": flops / ms / 1e9, "peak": tc_peak, "unit": "TFLOP/s",
-                   "kernel": "conv2d fprop 3x3 64->64 @56x56 b32", "ms": ms}
     return out
+
+
+def committed_traffic():
+    """DRAM bytes of the conv family per step from the committed ncu capture of one graph
+    replay (profiles/*/conv_traffic.json, newest round first), else None."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "conv_traffic.json")), reverse=True):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+            return d["dram_bytes_per_step"], os.path.relpath(path, ROOT)
+        except Exception:  # noqa: BLE001
+            continue
+    return None, None
+
+
+def launch_ranks(args):
+    """``--gpus N`` without a torchrun environment: start N ranks of this script through
+    torch.distributed.run on 127.0.0.1 and return its exit code (rank 0 prints the line)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -163,6 +289,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "RANK" not in os.environ and args.impl == "ours":
+        sys.exit(launch_ranks(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -175,13 +303,14 @@ def main():
             return
         cores = os.cpu_count()
         v, ms = cpu_reference(args.steps, args.warmup)
-        sample = f"ResNet-50 train_step at batch {REF_SAMPLE_BATCH} (bounded sample of the b32 workload)"
+        sample = (f"minml (the unmodified reference, baseline/_ref) EagerBackend ResNet-50 train_step at batch "
+                  f"{REF_SAMPLE_BATCH} (bounded sample of the b32 workload), {cores} threads on {cpu_model()}")
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
                           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-                          "data": "synthetic", "config": cfg,
-                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                                           "sample": sample},
+                          "data": "synthetic", "config": dict(cfg, sample_batch=REF_SAMPLE_BATCH),
+                          "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "reference",
+                                           "sample": sample, "cpu_model": cpu_model()},
                           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
 
@@ -304,16 +433,17 @@ def main():
     hbm, tc, src = peaks()
     rl = kernel_roofline(be, T, hbm, tc)
     dom = rl["conv"]
-    # traffic: dram read + write of the TMA conv kernel for this shape in one ncu --set full
-    # capture (profiles/r1/ncu_tma_conv_56x56.txt: 51.73 MB read + 1.60 MB written per launch;
-    # the hi/lo operand planes are read once, the output stays in L2 during the kernel)
+    traffic, traffic_src = committed_traffic()
     roofline = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
-                "frac": dom["achieved"] / dom["peak"], "traffic": 53.33e6, "traffic_unit": "bytes/launch",
-                "kernel": dom["kernel"], "peak_source": src,
-                "note": "achieved = useful FLOPs (2*N*F*Ho*Wo*C*kh*kw) / op time incl. the hi/lo pre-pass; "
-                        "3xTF32 issues 3 tf32 MMAs per useful MAC, so the useful ceiling is tf32 peak / 3",
+                "frac": dom["achieved"] / dom["peak"], "traffic": traffic, "traffic_unit": "DRAM bytes per step",
+                "traffic_source": traffic_src, "kernel": dom["kernel"], "peak_source": src,
+                "gflop_per_step": dom["gflop_per_step"], "ms_per_step": dom["ms_per_step"],
+                "ms_by_kind": dom["ms_by_kind"], "launches_per_step": dom["launches_per_step"],
+                "note": "achieved = useful FLOPs (2*N*F*Ho*Wo*C*kh*kw summed over the family) / summed op time "
+                        "(CUDA events, compute stream); 3xTF32 issues 3 tf32 MMAs per useful MAC, so the useful "
+                        "ceiling is the tf32 rate / 3 = bf16 peak / 6",
                 "frac_of_3xtf32_ceiling": dom["achieved"] / (tc / 2 / 3),
-                "other": {k: {kk: v for kk, v in d.items()} for k, d in rl.items() if k != "conv"}}
+                "other": {k: d for k, d in rl.items() if k != "conv"}}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights, N(0,1) images)",
@@ -327,9 +457,11 @@ def main():
         line["graph_error"] = graph_error
     if world == 1 and not args.no_cpu_baseline:
         v, ms = cpu_reference(2, 1)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"oracle ResNet-50 train_step at batch {REF_SAMPLE_BATCH}, 2 steps "
-                                          f"after 1 warm-up ({ms:.0f} ms/step)"}
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                                "cpu_model": cpu_model(),
+                                "sample": f"minml (unmodified reference) ResNet-50 train_step at batch "
+                                          f"{REF_SAMPLE_BATCH}, 2 steps after 1 warm-up ({ms:.0f} ms/step)",
+                                "per_op_overhead_us": cpu_overheads()}
     print(json.dumps(line))
 
 

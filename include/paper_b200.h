@@ -115,6 +115,11 @@ int pb_pad(const pb_tensor* src, const int64_t* lo, const pb_scalar* value, cons
 int pb_fill(const pb_tensor* out, const pb_scalar* value);                /* kernels.py:54-58 */
 int pb_arange(const pb_tensor* out);                                      /* kernels.py:61-62 */
 int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out); /* kernels.py:65-74, rng.py */
+/* pb_rand with counter offset = *(uint64_t*)base_ptr + delta read on the device: a fill recorded
+ * into a CUDA graph draws the counter range the host reserved for each replay
+ * (minml/_tensor.py:362-368 reserve, rng.py:16-51); pb_counter_add advances that counter. */
+int pb_rand_dev(int normal, uint64_t seed, uint64_t base_ptr, uint64_t delta, const pb_tensor* out);
+int pb_counter_add(uint64_t counter_ptr, uint64_t inc);
 int pb_reduce(int op, const pb_tensor* a, int axis /* -1 = all */, const pb_tensor* out); /* :139-160 */
 /* pb_reduce then out = op(result, scalar) (or op(scalar, result)) in f32, op in add/sub/mul/div:
    the reference's mean = sum / n (minml/ops.py:33-36) fused; backend-internal (planned fusion) */

@@ -95,13 +95,22 @@ class Manager {
     live_req_ -= b.requested;
     live_granted_ -= b.granted;
     cudaEvent_t ev = nullptr;
-    if (b.streams && !simulate_) {
-      // the block may still be read by another stream: park it behind an event
+    if (b.streams && !simulate_ && b.pool == 0) {
+      // the block may still be used by another stream: park it behind one event that
+      // completes after that stream's work queued so far.  Used on both side streams: the
+      // comm stream first waits for the copy stream's work, then records the event.
+      // (Graph-capture pools skip this: an event recorded inside a capture cannot be
+      // queried, and a recorded step joins its side streams before it ends.)
       cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-      for (int s = 1; s < 3; ++s)
-        if (b.streams & (1u << s)) {
-          cudaEventRecord(ev, s == 1 ? comm_stream() : copy_stream());
-        }
+      const bool on_comm = b.streams & 2u, on_copy = b.streams & 4u;
+      if (on_comm && on_copy) {
+        cudaEvent_t j = nullptr;
+        cudaEventCreateWithFlags(&j, cudaEventDisableTiming);
+        cudaEventRecord(j, copy_stream());
+        cudaStreamWaitEvent(comm_stream(), j, 0);
+        cudaEventDestroy(j);
+      }
+      cudaEventRecord(ev, on_comm ? comm_stream() : copy_stream());
     }
     if (policy_ == PB_POLICY_NATIVE) {
       ++free_count_;

@@ -23,14 +23,18 @@ static ncclDataType_t nccl_type(int dt) {
     if (r_ != ncclSuccess) return fail(PB_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
   } while (0)
 
-static int fence_compute_to_comm() {
-  cudaEvent_t ev;
-  PB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  PB_CUDA(cudaEventRecord(ev, compute_stream()));
-  PB_CUDA(cudaStreamWaitEvent(comm_stream(), ev, 0));
-  PB_CUDA(cudaEventDestroy(ev));
+// two persistent fence events (created once; a wait binds to the record before it, so one
+// event per direction can be re-recorded freely, also while a graph is being captured)
+static cudaEvent_t g_to_comm = nullptr, g_to_compute = nullptr;
+
+static int fence(cudaEvent_t* ev, cudaStream_t from, cudaStream_t to) {
+  if (!*ev) PB_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
+  PB_CUDA(cudaEventRecord(*ev, from));
+  PB_CUDA(cudaStreamWaitEvent(to, *ev, 0));
   return PB_OK;
 }
+
+static int fence_compute_to_comm() { return fence(&g_to_comm, compute_stream(), comm_stream()); }
 
 extern "C" {
 
@@ -85,12 +89,7 @@ int pb_nccl_allgather(void* comm, uint64_t send, uint64_t recv, uint64_t count, 
 
 int pb_nccl_wait(void* comm) {
   (void)comm;
-  cudaEvent_t ev;
-  PB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  PB_CUDA(cudaEventRecord(ev, comm_stream()));
-  PB_CUDA(cudaStreamWaitEvent(compute_stream(), ev, 0));
-  PB_CUDA(cudaEventDestroy(ev));
-  return PB_OK;
+  return fence(&g_to_compute, comm_stream(), compute_stream());
 }
 
 }  // extern "C"

@@ -20,14 +20,20 @@ __device__ __forceinline__ double unit(uint64_t seed, uint64_t counter) {
   return (double)(splitmix(seed, counter) >> 11) * 1.1102230246251565e-16;  // 2^-53
 }
 
+// `base` (may be null): a device-resident counter added to `offset` at run time, so a fill
+// recorded into a CUDA graph draws fresh counters on every replay (see pb_rand_dev)
 template <typename T>
-__global__ void __launch_bounds__(256) uniform_kernel(T* out, int64_t n, uint64_t seed, uint64_t offset) {
+__global__ void __launch_bounds__(256) uniform_kernel(T* out, int64_t n, uint64_t seed, uint64_t offset,
+                                                      const uint64_t* base) {
+  if (base) offset += *base;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (T)unit(seed, offset + (uint64_t)i);
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) normal_kernel(T* out, int64_t n, uint64_t seed, uint64_t offset) {
+__global__ void __launch_bounds__(256) normal_kernel(T* out, int64_t n, uint64_t seed, uint64_t offset,
+                                                     const uint64_t* base) {
+  if (base) offset += *base;
   int64_t pairs = (n + 1) / 2;
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < pairs; k += (int64_t)gridDim.x * blockDim.x) {
     double u1 = unit(seed, offset + (uint64_t)k);
@@ -43,7 +49,9 @@ __global__ void __launch_bounds__(256) normal_kernel(T* out, int64_t n, uint64_t
 
 using namespace pb;
 
-extern "C" int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out) {
+__global__ void counter_add_kernel(uint64_t* c, uint64_t inc) { *c += inc; }
+
+static int rand_fill(int normal, uint64_t seed, uint64_t offset, const uint64_t* base, const pb_tensor* out) {
   int64_t n = numel(*out);
   if (n == 0) return PB_OK;
   if (!is_contiguous(*out)) return fail(PB_ERR_ARG, "pb_rand: output must be contiguous");
@@ -51,14 +59,30 @@ extern "C" int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tens
   cudaStream_t s = compute_stream();
   void* p = (void*)(uintptr_t)out->ptr;
   if (out->dtype == PB_F32) {
-    if (normal) normal_kernel<float><<<grid, 256, 0, s>>>((float*)p, n, seed, offset);
-    else uniform_kernel<float><<<grid, 256, 0, s>>>((float*)p, n, seed, offset);
+    if (normal) normal_kernel<float><<<grid, 256, 0, s>>>((float*)p, n, seed, offset, base);
+    else uniform_kernel<float><<<grid, 256, 0, s>>>((float*)p, n, seed, offset, base);
   } else if (out->dtype == PB_F64) {
-    if (normal) normal_kernel<double><<<grid, 256, 0, s>>>((double*)p, n, seed, offset);
-    else uniform_kernel<double><<<grid, 256, 0, s>>>((double*)p, n, seed, offset);
+    if (normal) normal_kernel<double><<<grid, 256, 0, s>>>((double*)p, n, seed, offset, base);
+    else uniform_kernel<double><<<grid, 256, 0, s>>>((double*)p, n, seed, offset, base);
   } else {
     return fail(PB_ERR_ARG, "pb_rand: float outputs only");
   }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+extern "C" int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out) {
+  return rand_fill(normal, seed, offset, nullptr, out);
+}
+
+extern "C" int pb_rand_dev(int normal, uint64_t seed, uint64_t base_ptr, uint64_t delta, const pb_tensor* out) {
+  if (!base_ptr) return fail(PB_ERR_ARG, "pb_rand_dev: null counter");
+  return rand_fill(normal, seed, delta, (const uint64_t*)(uintptr_t)base_ptr, out);
+}
+
+extern "C" int pb_counter_add(uint64_t counter_ptr, uint64_t inc) {
+  if (!counter_ptr) return fail(PB_ERR_ARG, "pb_counter_add: null counter");
+  counter_add_kernel<<<1, 1, 0, compute_stream()>>>((uint64_t*)(uintptr_t)counter_ptr, inc);
   PB_LAUNCHED();
   return PB_OK;
 }

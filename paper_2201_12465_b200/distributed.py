@@ -42,20 +42,35 @@ class Communicator:
         self._seq = 0
 
     # ------------------------------------------------------------- plumbing
-    def _meta_check(self, kind, meta):
+    def _meta_check(self, kind, meta, publish=None):
+        """Compare (kind, meta) across ranks before any data moves (minml/distributed.py:
+        107-116).  Every rank posts ``meta/{seq}/{rank}`` and reads all peers'.  A rank that
+        has read every peer's post for ``seq`` knows every rank finished check ``seq - 1``,
+        so it deletes its own post of ``seq - 1``: the store holds at most two checks' keys.
+        ``publish`` (root only) is extra data peers read back from the root's post; the
+        root's value is returned on every rank."""
         seq = self._seq
         self._seq += 1
         if self.world_size == 1 or self._store is None:
-            return
+            return publish
         mine = repr((kind,) + tuple(meta))
-        self._store.set(f"meta/{seq}/{self.rank}", mine)
+        self._store.set(f"meta/{seq}/{self.rank}", mine + "\x00" + repr(publish))
+        extra = None
         for r in range(self.world_size):
             try:
-                peer = self._store.get(f"meta/{seq}/{r}").decode()
+                peer, _, pub = self._store.get(f"meta/{seq}/{r}").decode().partition("\x00")
             except Exception as exc:  # store timeout
                 raise CollectiveTimeout(f"rank {self.rank}: rank {r} missing from {kind} #{seq}: {exc}") from None
             if peer != mine:
                 raise CollectiveShapeError(f"rank {self.rank} called {mine}, rank {r} called {peer}")
+            if pub != "None":
+                extra = pub
+        if seq:
+            try:
+                self._store.delete_key(f"meta/{seq - 1}/{self.rank}")
+            except Exception:  # noqa: BLE001 -- a store without delete keeps the key
+                pass
+        return extra
 
     def _backend(self, tensor):
         return registry.get(tensor.backend_id)
@@ -73,10 +88,11 @@ class Communicator:
             return
         self._meta_check("barrier", ())
 
-    def all_reduce(self, tensor, op="sum"):
+    def all_reduce(self, tensor, op="sum", _checked=False):
         if op not in ("sum", "max"):
             raise ValueError(f"all_reduce op must be 'sum' or 'max', got {op!r}")
-        self._meta_check("all_reduce", (tuple(tensor.shape), tensor.dtype.name, op))
+        if not _checked:
+            self._meta_check("all_reduce", (tuple(tensor.shape), tensor.dtype.name, op))
         if self.world_size == 1:
             return tensor
         if self._device(tensor):
@@ -102,11 +118,28 @@ class Communicator:
         return T.tensor(np.stack([o.numpy() for o in outs]), backend=tensor.backend_id)
 
     def broadcast(self, tensor, root=0):
+        """Root's tensor on every rank (minml/distributed.py:166-175): only ``root`` is
+        compared across ranks; the root publishes shape, dtype and backend, so other ranks
+        may pass ``None`` or a placeholder of any shape."""
         if not 0 <= root < self.world_size:
             raise ValueError(f"root {root} outside world of {self.world_size}")
-        self._meta_check("broadcast", (root, tuple(tensor.shape), tensor.dtype.name))
+        mine = None
+        if self.rank == root:
+            if tensor is None:
+                raise ValueError("broadcast: the root must pass a tensor")
+            mine = (tuple(tensor.shape), tensor.dtype.name, tensor.backend_id)
+        pub = self._meta_check("broadcast", (root,), publish=mine)
         if self.world_size == 1:
             return tensor
+        import ast
+        shape, dtname, root_backend = ast.literal_eval(pub) if isinstance(pub, str) else pub
+        if self.rank != root:
+            if tensor is not None:
+                backend = tensor.backend_id
+            else:
+                backend = root_backend if root_backend in registry.registered_ids() else registry.default().name
+            if tensor is None or tuple(tensor.shape) != shape or tensor.dtype.name != dtname:
+                tensor = T.zeros(shape, dtype=dtname, backend=backend)
         if self._device(tensor):
             return self._backend(tensor).nccl_broadcast(self._nccl, tensor, root)
         import torch
@@ -132,14 +165,26 @@ def init_from_env(device_backend=True, timeout=DEFAULT_TIMEOUT):
         store = dist.distributed_c10d._get_default_store()
         return Communicator(rank, world, store=store, gloo=True, timeout=timeout)
     store = dist.TCPStore(addr, port + 1, world, rank == 0, timeout=datetime.timedelta(seconds=timeout))
+    if rank == 0:
+        store.set("nccl_id", nccl_unique_id())
+    return nccl_communicator(rank, world, store.get("nccl_id"), store=store, timeout=timeout)
+
+
+def nccl_unique_id():
+    """128 bytes of ncclUniqueId from rank 0 (pb_nccl_unique_id)."""
+    import ctypes
+    from .gpu import _lib
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.load().pb_nccl_unique_id(buf), "nccl id")
+    return buf.raw
+
+
+def nccl_communicator(rank, world, uid, store=None, timeout=DEFAULT_TIMEOUT):
+    """A Communicator over an NCCL communicator in libpaper_b200.so (``world`` may be 1:
+    the device data plane -- bucket packing, ncclAllReduce on the comm stream, the
+    compute<->comm fences -- then runs for real on a single GPU)."""
     from .gpu import _lib
     lib = _lib.load()
-    if rank == 0:
-        import ctypes
-        buf = ctypes.create_string_buffer(128)
-        _lib.check(lib.pb_nccl_unique_id(buf), "nccl id")
-        store.set("nccl_id", buf.raw)
-    uid = store.get("nccl_id")
     comm = lib.pb_nccl_init(world, rank, uid)
     if not comm:
         raise RuntimeError(lib.pb_last_error().decode())
@@ -147,11 +192,14 @@ def init_from_env(device_backend=True, timeout=DEFAULT_TIMEOUT):
 
 
 def data_parallel_sync(comm, params):
-    """grad <- all_reduce(grad, 'sum') / world for every parameter (reference semantics)."""
+    """grad <- all_reduce(grad, 'sum') / world for every parameter (reference semantics,
+    minml/distributed.py:216-222); one metadata exchange covers the whole parameter list."""
     for i, p in enumerate(params):
         if p.grad is None:
             raise MissingGradient(f"parameter {i} has no gradient to synchronize")
-        p.grad = comm.all_reduce(p.grad, "sum") / comm.world_size
+    comm._meta_check("dp_sync", tuple((tuple(p.grad.shape), p.grad.dtype.name) for p in params))
+    for p in params:
+        p.grad = comm.all_reduce(p.grad, "sum", _checked=True) / comm.world_size
 
 
 class DataParallel:
@@ -178,12 +226,11 @@ class DataParallel:
         comm._meta_check("ddp_plan", tuple((tuple(p.shape), p.dtype.name) for p in self.params))
 
     def backward(self, loss):
-        if self.comm.world_size == 1:
-            loss.backward()
+        if self.comm.world_size == 1 and self.comm._nccl is None:
+            loss.backward()  # one rank, no communicator: grad / 1 == grad, nothing to do
             for p in self.params:
                 if p.grad is None:
                     raise MissingGradient("parameter has no gradient to synchronize")
-                p.grad = p.grad / 1
             return
         pending = [len(b) for b in self.buckets]
         flights = {}
@@ -219,18 +266,22 @@ class DataParallel:
                 raise MissingGradient(f"parameter {i} has no gradient to synchronize")
             grads.append(g)
         be = registry.get(grads[0].backend_id)
-        if hasattr(be, "bucket_pack"):
+        if hasattr(be, "bucket_pack") and all(g.dtype.name == "f32" for g in grads):
             flat = be.bucket_pack(grads)
         else:
             flat = T.concat([g.reshape((g.shape.size,)) for g in grads], 0)
-        return self.comm.all_reduce(flat, "sum") if self.comm._nccl is None else \
-            be.nccl_all_reduce(self.comm._nccl, flat, "sum", wait=False)
+        if self.comm._nccl is not None and hasattr(be, "nccl_all_reduce"):
+            # ncclAvg: sum and the exact power-of-two 1/world scale in the collective itself
+            avg = self.comm.world_size & (self.comm.world_size - 1) == 0
+            return be.nccl_all_reduce(self.comm._nccl, flat, "avg" if avg else "sum", wait=False), avg
+        return self.comm.all_reduce(flat, "sum", _checked=True), False
 
-    def _finish(self, b, reduced):
+    def _finish(self, b, flight):
+        reduced, averaged = flight
         be = registry.get(reduced.backend_id)
         if hasattr(be, "nccl_wait") and self.comm._nccl is not None:
             be.nccl_wait(self.comm._nccl)
-        avg = reduced / self.comm.world_size
+        avg = reduced if averaged else reduced / self.comm.world_size
         off = 0
         for i in self.buckets[b]:
             p = self.params[i]

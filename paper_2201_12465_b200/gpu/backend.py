@@ -16,9 +16,10 @@ backend cannot be constructed.
 """
 
 import ctypes
-import weakref
 import os
 import sys
+import threading
+import weakref
 
 import numpy as np
 
@@ -228,15 +229,39 @@ _EPI = {"add", "sub", "mul", "div"}
 
 
 class GraphExec:
-    """An instantiated CUDA graph of compute-stream work (see GpuBackend.capture_begin)."""
+    """An instantiated CUDA graph of compute-stream work (see GpuBackend.capture_begin).
 
-    __slots__ = ("backend", "handle")
+    Random fills recorded into the graph (dropout masks) read their counter offset from a
+    device-resident counter (``pb_rand_dev``) that the graph's last kernel advances by the
+    counters one replay consumes.  Every replay after the first reserves that many counters
+    from the backend's host ``RngState`` -- the reservation the eager step would have made
+    (minml/_tensor.py:362-368) -- so the stream of masks, and the host counter, are those of
+    the same number of eager steps.  If anything else reserved counters in between, the
+    device counter is rewritten (stream-ordered) before the launch."""
 
-    def __init__(self, backend, handle):
+    __slots__ = ("backend", "handle", "rng_counter", "rng_per_step", "rng_seed", "rng_next", "__weakref__")
+
+    def __init__(self, backend, handle, rng=None):
         self.backend = backend
         self.handle = handle
+        self.rng_counter = None
+        self.rng_per_step = 0
+        if rng is not None:
+            self.rng_counter, self.rng_per_step, self.rng_seed, self.rng_next = rng
 
     def launch(self):
+        if self.rng_per_step:
+            be = self.backend
+            if be.rng.seed != self.rng_seed:
+                raise DeviceError("the backend was reseeded after this graph recorded random fills; record it again")
+            if self.rng_next is None:  # first replay: the recording step reserved its counters
+                self.rng_next = be.rng.state()["next"]
+            else:
+                off = be.rng.reserve(self.rng_per_step)
+                if off != self.rng_next:
+                    v = np.array([off], dtype=np.uint64)
+                    _lib.check(be._lib.pb_h2d(self.rng_counter.ptr, v.ctypes.data, 8), "rng counter")
+                self.rng_next = off + self.rng_per_step
         _lib.check(self.backend._lib.pb_graph_launch(self.handle), "graph launch")
 
     def __del__(self):
@@ -251,6 +276,8 @@ class GpuBackend(Backend):
 
     def __init__(self, name="gpu", seed=0, device=0, fuse=None):
         self._capture_pool = 0
+        self._cap_rng = None
+        self._lock = threading.RLock()
         # backend-internal elementwise fusion, opt-in (PB_FUSE=1 or fuse=True):
         # bit-identical (tests/test_gpu_fusion.py) but the interpreted chain kernel is still
         # ALU-bound -- ResNet-50 measured 576 samples/s fused vs 634 unfused
@@ -314,6 +341,10 @@ class GpuBackend(Backend):
         return old
 
     def _alloc(self, nbytes, opname):
+        with self._lock:
+            return self._alloc_locked(nbytes, opname)
+
+    def _alloc_locked(self, nbytes, opname):
         try:
             h, ledger = self._mm
         except AttributeError:
@@ -350,9 +381,15 @@ class GpuBackend(Backend):
 
     # ----------------------------------------------------------------- execute
     def execute(self, call, args):
-        if self._trace is not None or self._planned:
-            return self._execute_traced(call, args)
-        return self._execute(call, args)
+        # concurrency ("execute may be called concurrently"): one re-entrant lock
+        # serialises the host side of each primitive -- the shared allocation result block,
+        # the device flag of the domain checks, the fill cache -- while launches stay
+        # asynchronous on the one compute stream, whose order makes any handle a thread
+        # receives safe to consume.  Tracing / recording a CUDA graph is single-threaded.
+        with self._lock:
+            if self._trace is not None or self._planned:
+                return self._execute_traced(call, args)
+            return self._execute(call, args)
 
     def _execute(self, call, args):
         name = call.name
@@ -470,6 +507,12 @@ class GpuBackend(Backend):
             raise DeviceError("a capture is already in progress")
         self.synchronize()
         h, _ = self._bind_or_get()
+        # device-resident RNG counter for random fills recorded into this graph (GraphExec)
+        base = self.rng.state()["next"]
+        blk = self._alloc(8, "rng_counter")
+        v = np.array([base], dtype=np.uint64)
+        _lib.check(self._lib.pb_h2d(blk.ptr, v.ctypes.data, 8), "rng counter")
+        self._cap_rng = [blk, base, self.rng.seed, 0]
         GpuBackend._next_pool += 1
         self._capture_pool = GpuBackend._next_pool
         self._lib.pb_mm_pool(h, self._capture_pool)
@@ -483,12 +526,23 @@ class GpuBackend(Backend):
         """Finish the recording; returns a ``GraphExec`` whose ``launch()`` replays it."""
         h, _ = self._bind_or_get()
         ex = ctypes.c_uint64(0)
+        blk, base, seed, nrand = self._cap_rng
+        rng = None
         try:
-            _lib.check(self._lib.pb_graph_end(ctypes.byref(ex)), "graph capture")
+            if nrand:
+                if self.rng.seed != seed:
+                    raise DeviceError("the backend was reseeded while recording a CUDA graph")
+                per_step = self.rng.state()["next"] - base
+                _lib.check(self._lib.pb_counter_add(blk.ptr, per_step), "rng counter")
+                rng = (blk, per_step, seed, None)
         finally:
-            self._lib.pb_mm_pool(h, 0)
-            self._capture_pool = 0
-        return GraphExec(self, ex.value)
+            try:
+                _lib.check(self._lib.pb_graph_end(ctypes.byref(ex)), "graph capture")
+            finally:
+                self._lib.pb_mm_pool(h, 0)
+                self._capture_pool = 0
+                self._cap_rng = None
+        return GraphExec(self, ex.value, rng)
 
     @property
     def capturing(self):
@@ -614,15 +668,22 @@ class GpuBackend(Backend):
         return out
 
     def _rand(self, call, args):
-        if self._capture_pool:
-            # the counter offset is reserved on the host (minml/_tensor.py:362-368): a replay
-            # would repeat this draw, so random ops stay out of graphs
-            raise DeviceError(f"{call.name} cannot be recorded into a CUDA graph (host-reserved RNG counter)")
         out = self._new(tuple(call.shape), call.dtype, call.name)
         if out.block is not None:
             p = call.params
-            _lib.check(self._lib.pb_rand(1 if call.name == "rand_normal" else 0, p["seed"] & ((1 << 64) - 1),
-                                         p["offset"], out.packed()), call.name)
+            kind = 1 if call.name == "rand_normal" else 0
+            seed = p["seed"] & ((1 << 64) - 1)
+            if self._capture_pool:
+                # recorded: the offset is relative to the graph's device counter (GraphExec),
+                # so each replay draws the counters the host reserves for it
+                cap = self._cap_rng
+                if seed != cap[2] or p["offset"] < cap[1]:
+                    raise DeviceError(f"{call.name} with a foreign seed/counter cannot be recorded into a CUDA graph")
+                cap[3] += 1
+                _lib.check(self._lib.pb_rand_dev(kind, seed, cap[0].ptr, p["offset"] - cap[1], out.packed()),
+                           call.name)
+            else:
+                _lib.check(self._lib.pb_rand(kind, seed, p["offset"], out.packed()), call.name)
         return out
 
     def _from_host(self, call, args):
@@ -984,6 +1045,9 @@ class GpuBackend(Backend):
 
     def bucket_pack(self, grads):
         """Concatenate flattened f32 gradients into one bucket with a single launch."""
+        for g in grads:
+            if g.dtype.name != "f32":
+                raise DTypeError(f"bucket_pack packs f32 gradients only, got {g.dtype.name}")
         n = len(grads)
         srcs = (ctypes.c_uint64 * n)()
         numel = (ctypes.c_int64 * n)()
@@ -998,15 +1062,26 @@ class GpuBackend(Backend):
         _lib.check(self._lib.pb_bucket_pack(n, srcs, numel, out.ptr), "bucket_pack")
         return self._tensor(out, (total,))
 
+    _NCCL_OPS = {"sum": 0, "max": 1, "avg": 2}
+
     def nccl_all_reduce(self, comm, tensor, op="sum", wait=True):
+        """ncclAllReduce on the comm stream (after a compute->comm fence).  ``op`` "avg" is
+        ncclAvg: for the power-of-two worlds of one node the 1/N scale is exact, so it equals
+        the reference's sum-then-divide (minml/distributed.py:216-222) bit for bit.  With
+        ``wait=False`` the compute stream is not joined: call ``nccl_wait`` before reading
+        the result; the source stays referenced until then, and both blocks are recorded
+        on the comm stream so an early free parks them behind a comm-stream event."""
         a = self._contig(tensor.adapter)
         out = self._new(a.shape, a.dtype, "all_reduce")
         _lib.check(self._lib.pb_nccl_allreduce(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code,
-                                               0 if op == "sum" else 1), "ncclAllReduce")
+                                               self._NCCL_OPS[op]), "ncclAllReduce")
         if wait:
             self.nccl_wait(comm)
         else:
             out.host = None
+            for blk in (a.block, out.block):
+                if blk is not None:
+                    _lib.check(self._lib.pb_mm_record_stream(blk.mm, blk.id, 1), "record_stream")
             self._inflight = getattr(self, "_inflight", [])
             self._inflight.append(a)  # source must outlive the collective
         return self._tensor(out, tuple(tensor.shape))

@@ -77,12 +77,23 @@ class CapturedStep:
 
     State the step rebinds instead of updating in place (e.g. BatchNorm running stats,
     minml/nn.py:299-300) is copied back into its original buffer at the end of the graph,
-    so every replay reads the previous replay's state.  Random primitives (dropout) cannot
-    be recorded: their counter offset is reserved on the host per call.
+    so every replay reads the previous replay's state.  Random primitives (dropout) read
+    their counter offset from a device counter that each replay advances by the range the
+    host reserves for it (GpuBackend ``GraphExec``), so masks match the eager steps'.
+
+    Only ``optim.SGD`` is recorded: its hyper-parameters are kernel scalars, so a change of
+    ``lr`` / ``momentum`` / ``weight_decay`` -- or parameters / velocities rebound from
+    outside (a checkpoint restore) -- makes the next call record the step again.  Adam keeps
+    its step count and bias corrections on the host and rebinds its moments every step, so
+    it is refused (``TypeError``) rather than replayed wrong.
     """
 
     def __init__(self, model, optimizer, ddp=None, warmup=2, fuse=True):
+        if type(optimizer) is not optim.SGD:
+            raise TypeError(f"CapturedStep records optim.SGD steps only, not {type(optimizer).__name__} "
+                            "(use training.train_step)")
         self.model, self.opt, self.ddp = model, optimizer, ddp
+        self._sig = None
         self.backend = registry.get(model_backend(model))
         self.warmup = int(warmup)
         # trace-planned elementwise fusion: the last warm-up step is traced, the recorded
@@ -160,10 +171,18 @@ class CapturedStep:
                 if trace:
                     self.fused_ops = be.fusion_trace_end()
             return loss.scalar(), out
+        if self.graph is not None and self._signature() != self._sig:
+            self.graph = None  # hyper-parameters or state buffers changed: record again
         if self.graph is None:
             self._capture()
         self.graph.launch()
         return self.loss.scalar(), self.out
+
+    def _signature(self):
+        o = self.opt
+        vel = o.velocity or ()
+        return (o.lr, o.momentum, o.weight_decay, tuple(p.data.adapter.ptr for p in o.params),
+                tuple(v.adapter.ptr for v in vel))
 
     def run(self, batches):
         """Pipelined steps over an iterable of host ``(images, labels)`` batches; yields each
@@ -180,6 +199,11 @@ class CapturedStep:
         be = self.backend
         pending, k = None, 0
         for images, labels in batches:
+            if self.graph is not None and self._signature() != self._sig:
+                if pending is not None:
+                    yield float(be.fetch_read(*pending).reshape(()))
+                    pending = None
+                self.graph = None
             if self.graph is None:
                 yield self(images, labels)[0]
                 continue
@@ -254,6 +278,7 @@ class CapturedStep:
                 self._fills = be.fill_cache_end()  # blocks the graph reads: kept with it
         self.launches = be.launch_count() - n0  # kernels recorded into the graph (per replay)
         self.loss, self.out = loss, out
+        self._sig = self._signature()
 
 
 # ---------------------------------------------------------------------- checkpoints

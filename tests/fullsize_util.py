@@ -1,0 +1,68 @@
+"""The five BASELINE.json configs at full width and depth, run through the product front end
+on any registered backend, against the reference's own 10-step trajectories
+(tests/golden/fullsize.*, made by tests/golden/make_fullsize_golden.py)."""
+
+import json
+import os
+
+import numpy as np
+
+import inputs as GI
+from paper_2201_12465_b200 import models as PM
+from paper_2201_12465_b200 import optim, training
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+BUILDERS = {
+    "mlp_full": (lambda be: PM.mlp(784, 256, 10, backend=be), (784,), 10, None),
+    "lenet_full": (lambda be: PM.mnist_cnn(backend=be), (1, 28, 28), 10, None),
+    "alexnet_full": (lambda be: PM.alexnet(backend=be), (3, 224, 224), 1000, None),
+    "resnet50_full": (lambda be: PM.resnet50(backend=be), (3, 224, 224), 1000, None),
+    "bert_full": (lambda be: PM.bert_base(backend=be), None, 2, (128, 30522)),
+}
+
+
+def meta():
+    with open(os.path.join(GOLD, "fullsize.json")) as f:
+        return json.load(f)
+
+
+def arrays():
+    return np.load(os.path.join(GOLD, "fullsize.npz"))
+
+
+def batches(name, batch):
+    _, shape, classes, tokens = BUILDERS[name]
+    return [GI.batch(name, k, shape, classes, batch, tokens=tokens) for k in range(2)]
+
+
+def run(name, m, backend, mode="eager"):
+    """10 steps of ``train_step`` (mode "eager") or of ``CapturedStep(fuse=True).run``
+    (mode "graph": 2 eager warm-up steps, then graph replays with pipelined host copies).
+    Returns (losses, params as host arrays)."""
+    backend.seed(m["seed"])
+    model = BUILDERS[name][0](backend.name)
+    opt = optim.SGD(model.params(), **m["sgd"])
+    bs = batches(name, m["batch"])
+    if mode == "eager":
+        losses = [training.train_step(model, *bs[k % 2], opt)[0] for k in range(m["steps"])]
+    else:
+        step = training.CapturedStep(model, opt, warmup=2, fuse=True)
+        losses = list(step.run(bs[k % 2] for k in range(m["steps"])))
+        assert step.graph is not None
+    return losses, [p.numpy() for p in model.params()]
+
+
+def compare(name, m, arr, losses, params):
+    """Errors under the reference's metric |a-b|/max(|a|,|b|,1) (T/test_acceptance.py:260-262):
+    losses, per-parameter signed sums and sum|p|, and the sampled parameter elements."""
+    from golden_util import rel_err
+    sums = [[float(np.sum(p, dtype=np.float64)), float(np.sum(np.abs(p), dtype=np.float64))] for p in params]
+    sampled = 0.0
+    for i, p in enumerate(params):
+        idx, val = arr[f"{name}_p{i}_idx"], arr[f"{name}_p{i}_val"]
+        sampled = max(sampled, rel_err(p.reshape(-1)[idx], val))
+    return {"loss": rel_err(losses, m["losses"]),
+            "sum": rel_err([s for s, _ in sums], [s for s, _ in m["param_sums"]]),
+            "abs_sum": rel_err([a for _, a in sums], [a for _, a in m["param_sums"]]),
+            "sampled": sampled}

@@ -32,3 +32,14 @@ def test_trajectory_matches_reference(name, oracle_backend):
         key = f"{name}_p{i}"
         if key in arrays.files:
             assert rel_err(p.numpy(), arrays[key]) <= 1e-5, key
+
+
+@pytest.mark.parametrize("name", ["mlp_full", "lenet_full"])
+def test_fullsize_oracle_matches_reference(name, oracle_backend):
+    """The oracle pinned at BASELINE size too (configs 1-2 at their real batch, 10 steps):
+    the checker the GPU full-size tests are read against agrees with the reference run."""
+    from fullsize_util import arrays, compare, meta, run
+    m = meta()[name]
+    losses, params = run(name, m, oracle_backend, "eager")
+    err = compare(name, m, arrays(), losses, params)
+    assert err["loss"] <= 1e-6 and err["sum"] <= 1e-6 and err["sampled"] <= 1e-6, err

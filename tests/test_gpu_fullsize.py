@@ -1,0 +1,43 @@
+"""North-star parity at BASELINE.json sizes: all five configs, full width and depth, train
+10 steps on the B200 -- through the eager ``train_step`` and through the benched path
+(``CapturedStep(fuse=True).run``: planned fusion + CUDA graph + pipelined host copies) --
+and match the reference's own CPU run on the same inputs and seeds
+(tests/golden/fullsize.*, minml EagerBackend, make_fullsize_golden.py).
+
+Tolerances, all under the reference's metric |a-b|/max(|a|,|b|,1)
+(T/test_acceptance.py:260-262):
+  * losses: 1e-3 over the 10 steps (BASELINE.json north_star);
+  * every parameter's signed sum and sum|p|: 1e-3;
+  * 64 sampled elements of every parameter: 1e-4.
+The measured errors are written to gpurun_out/fullsize_parity.jsonl."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from fullsize_util import BUILDERS, arrays, compare, meta, run
+from gpu_util import gpu_backend
+
+pytestmark = pytest.mark.gpu
+META = meta()
+ARR = arrays()
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+@pytest.mark.parametrize("mode", ["eager", "graph"])
+@pytest.mark.parametrize("name", list(BUILDERS))
+def test_fullsize_config_matches_reference(name, mode):
+    be = gpu_backend()
+    m = META[name]
+    losses, params = run(name, m, be, mode)
+    err = compare(name, m, ARR, losses, params)
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, "fullsize_parity.jsonl"), "a") as f:
+        f.write(json.dumps({"config": name, "mode": mode, "batch": m["batch"], "errors": err,
+                            "losses": losses, "ref_losses": m["losses"]}) + "\n")
+    assert err["loss"] <= 1e-3, (err, losses, m["losses"])
+    assert err["sum"] <= 1e-3 and err["abs_sum"] <= 1e-3, err
+    assert err["sampled"] <= 1e-4, err
+    assert all(np.isfinite(p).all() for p in params)

@@ -7,7 +7,7 @@ import pytest
 
 from frontend_util import BUILDERS
 from gpu_util import gpu_backend
-from paper_2201_12465_b200 import errors, models, optim, training
+from paper_2201_12465_b200 import models, optim, training
 
 pytestmark = pytest.mark.gpu
 
@@ -70,18 +70,50 @@ def test_planned_fusion_bit_identical_and_fewer_launches(name, shape, classes):
         assert np.array_equal(a, b)
 
 
-def test_captured_step_rejects_dropout_and_bad_targets():
+@pytest.mark.parametrize("fuse", [False, True])
+def test_captured_dropout_draws_fresh_masks_bit_identical(fuse):
+    """Dropout (minml/nn.py:247-256) inside the graph: each replay draws the counter range the
+    host reserves for it (pb_rand_dev + GraphExec), so the masks, losses, parameters and the
+    host RNG counter equal those of the same number of eager steps."""
+    be = gpu_backend()
+    eager = _run("alexnet_tiny", be, False, 6, 4, (3, 67, 67), 10)
+    eager_next = be.rng.state()["next"]
+    graph = _run("alexnet_tiny", be, True, 6, 4, (3, 67, 67), 10, fuse=fuse)
+    assert graph[4].graph is not None and graph[4].graph.rng_per_step > 0
+    assert be.rng.state()["next"] == eager_next
+    assert eager[0] == graph[0], (eager[0], graph[0])
+    for a, b in zip(eager[1] + eager[2], graph[1] + graph[2]):
+        assert np.array_equal(a, b)
+
+
+def test_captured_dropout_follows_foreign_reservations():
+    """An eager random draw between replays moves the host counter; the next replay rewrites
+    the device counter and still draws exactly what the eager step would."""
+    from paper_2201_12465_b200 import _tensor as T
+    be = gpu_backend()
+    runs = []
+    for captured in (False, True):
+        be.seed(9)
+        model = BUILDERS["alexnet_tiny"](be.name)
+        opt = optim.SGD(model.params(), lr=0.01)
+        r = np.random.default_rng(1)
+        x = r.standard_normal((2, 3, 67, 67)).astype(np.float32)
+        y = r.integers(0, 10, 2).astype(np.int64)
+        step = training.CapturedStep(model, opt, warmup=1, fuse=False) if captured else None
+        losses = []
+        for k in range(5):
+            if k == 3:
+                T.rand_uniform((7,), backend=be.name)  # a foreign reservation
+            losses.append(step(x, y)[0] if captured else training.train_step(model, x, y, opt)[0])
+        runs.append((losses, [p.numpy() for p in model.params()]))
+    assert runs[0][0] == runs[1][0]
+    for a, b in zip(runs[0][1], runs[1][1]):
+        assert np.array_equal(a, b)
+
+
+def test_captured_step_checks_targets():
     be = gpu_backend()
     be.seed(1)
-    model = models.alexnet(classes=10, image=67, channels=(8, 16, 24, 16, 16), hidden=64, backend=be.name)
-    opt = optim.SGD(model.params(), lr=0.01)
-    step = training.CapturedStep(model, opt, warmup=1)
-    x = np.zeros((2, 3, 67, 67), np.float32)
-    y = np.zeros(2, np.int64)
-    step(x, y)  # eager warm-up is fine
-    with pytest.raises(errors.DeviceError):
-        step(x, y)  # recording a dropout mask is refused
-    be.synchronize()
     lenet = models.mnist_cnn(backend=be.name)
     st = training.CapturedStep(lenet, optim.SGD(lenet.params(), lr=0.01), warmup=1)
     xs = np.zeros((2, 1, 28, 28), np.float32)
