@@ -120,6 +120,9 @@ int pb_rand(int normal, uint64_t seed, uint64_t offset, const pb_tensor* out); /
  * (minml/_tensor.py:362-368 reserve, rng.py:16-51); pb_counter_add advances that counter. */
 int pb_rand_dev(int normal, uint64_t seed, uint64_t base_ptr, uint64_t delta, const pb_tensor* out);
 int pb_counter_add(uint64_t counter_ptr, uint64_t inc);
+/* test probe: out[i] = a[i] / b[i] by the reciprocal + exact-residual path the per-row
+ * broadcast kernel uses (must equal IEEE division bit for bit) */
+int pb_fastdiv_probe(uint64_t a, uint64_t b, uint64_t out, int64_t n);
 int pb_reduce(int op, const pb_tensor* a, int axis /* -1 = all */, const pb_tensor* out); /* :139-160 */
 /* pb_reduce then out = op(result, scalar) (or op(scalar, result)) in f32, op in add/sub/mul/div:
    the reference's mean = sum / n (minml/ops.py:33-36) fused; backend-internal (planned fusion) */

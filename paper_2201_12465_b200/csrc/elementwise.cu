@@ -332,6 +332,94 @@ __global__ void __launch_bounds__(256) ew_bc1(BcArgs p, float sa, float sb) {
 }
 
 
+// ------------------------------------------------ per-row broadcast (BatchNorm's pattern)
+// out[e] = op(D[e], R[row(e)]) or op(R[row(e)], D[e]) where D is dense in the output's own
+// layout and R holds one value per output row (inner stride 0): x - mean, x / std, x * gamma,
+// x + beta over [N,C,H,W] with [1,C,1,1] operands.  All index math is 32-bit: one FastDiv for
+// the row of each float4, up to three more for R's offset.  A row-broadcast divisor gets its
+// IEEE reciprocal once per float4 and each quotient one exact-residual correction
+// (div_rn_rcp), which is the correctly rounded a / b.
+struct ChanArgs {
+  const float* d;
+  const float* r;
+  void* out;
+  uint32_t n4;        // float4s in the output
+  FastDiv row_len;    // inner (row) extent, % 4 == 0
+  int nouter;         // outer coalesced axes (<= 3)
+  FastDiv ext[3];     // their extents, outermost first
+  uint32_t rs[3];     // R's element strides along them
+};
+
+// a / b correctly rounded, given r = RN(1/b) (Markstein: q = RN(a*r) is within one ulp of
+// a/b, the residual a - q*b is exact with one FMA, and RN(q + residual*r) is RN(a/b)).  The
+// theorem needs every intermediate normal: operands outside [2^-60, 2^60] (zeros, subnormals,
+// inf, NaN included) take the IEEE division instead.  Checked bit for bit against IEEE
+// division in tests/test_gpu_ops.py::test_fast_division_is_ieee_exact.
+__device__ __forceinline__ float div_rn_rcp(float a, float b, float r) {
+  const float aa = fabsf(a), ab = fabsf(b);
+  if (aa >= 0x1p-60f && aa <= 0x1p60f && ab >= 0x1p-60f && ab <= 0x1p60f) {
+    const float q = __fmul_rn(a, r);
+    const float e = __fmaf_rn(-q, b, a);
+    return __fmaf_rn(e, r, q);
+  }
+  return a / b;
+}
+
+template <int OP, int RLEFT>
+__global__ void __launch_bounds__(256) ew_chan4(ChanArgs p) {
+  typedef typename Bin<OP, float>::res R;
+  typedef typename Out4<R>::type O4;
+  const uint32_t step = gridDim.x * 1024u;
+  for (uint32_t base = blockIdx.x * 1024u + threadIdx.x; base < p.n4; base += step) {
+    float4 xd[4];
+    float xr[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t v = base + u * 256u;
+      xd[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      xr[u] = 1.f;
+      if (v < p.n4) {
+        uint32_t row = p.row_len.div(v * 4u), off = 0;
+#pragma unroll
+        for (int k = 2; k >= 0; --k) {
+          if (k < p.nouter) {
+            uint32_t q, rr;
+            p.ext[k].divmod(row, q, rr);
+            off += rr * p.rs[k];
+            row = q;
+          }
+        }
+        xd[u] = __ldg(reinterpret_cast<const float4*>(p.d) + v);
+        xr[u] = __ldg(p.r + off);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t v = base + u * 256u;
+      if (v >= p.n4) continue;
+      const float4 a = xd[u];
+      const float b = xr[u];
+      if (OP == PB_DIV && !RLEFT) {
+        const float rc = __frcp_rn(b);
+        reinterpret_cast<float4*>(p.out)[v] =
+            make_float4(div_rn_rcp(a.x, b, rc), div_rn_rcp(a.y, b, rc), div_rn_rcp(a.z, b, rc), div_rn_rcp(a.w, b, rc));
+      } else if (RLEFT) {
+        reinterpret_cast<O4*>(p.out)[v] = mk4(Bin<OP, float>::f(b, a.x), Bin<OP, float>::f(b, a.y),
+                                              Bin<OP, float>::f(b, a.z), Bin<OP, float>::f(b, a.w));
+      } else {
+        reinterpret_cast<O4*>(p.out)[v] = mk4(Bin<OP, float>::f(a.x, b), Bin<OP, float>::f(a.y, b),
+                                              Bin<OP, float>::f(a.z, b), Bin<OP, float>::f(a.w, b));
+      }
+    }
+  }
+}
+
+// exact-division probe for the tests: out[i] = div_rn_rcp(a[i], b[i], RN(1/b[i]))
+__global__ void fastdiv_probe(const float* a, const float* b, float* out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = div_rn_rcp(a[i], b[i], __frcp_rn(b[i]));
+}
+
 // ------------------------------------------------------------- fused elementwise chains
 // Backend-internal fusion (the rule of minml/deferred.py:146-163 restated for
 // the GPU): the backend defers f32/bool elementwise primitives and runs a whole linear
@@ -852,6 +940,42 @@ static int try_bcast_f32(const pb_tensor* a, const pb_tensor* b, float sa, float
     }
   }
   cudaStream_t s = compute_stream();
+  if (v4 && a && b && d.ndim >= 2 && d.ndim <= 4) {
+    // one operand dense in the output's layout, the other constant along each row
+    int dense = -1;
+    for (int o = 0; o < 2; ++o) {
+      bool same = true;
+      int64_t acc = 1;
+      for (int k = d.ndim - 1; k >= 0; --k) {
+        if (d.st[o][k] != acc) same = false;
+        acc *= d.shape[k];
+      }
+      if (same && d.st[1 - o][in] == 0) dense = o;
+    }
+    bool small = dense >= 0;
+    for (int k = 0; small && k < in; ++k)
+      if (d.st[1 - dense][k] < 0 || d.st[1 - dense][k] >= ((int64_t)1 << 30)) small = false;
+    if (small) {
+      ChanArgs c;
+      c.d = dense == 0 ? p.a : p.b;
+      c.r = dense == 0 ? p.b : p.a;
+      c.out = p.out;
+      c.n4 = (uint32_t)(n / 4);
+      c.row_len = FastDiv((uint32_t)d.shape[in]);
+      c.nouter = in;
+      for (int k = 0; k < 3; ++k) {
+        c.ext[k] = FastDiv(k < in ? (uint32_t)d.shape[k] : 1u);
+        c.rs[k] = k < in ? (uint32_t)d.st[1 - dense][k] : 0u;
+      }
+      int grid = grid_for(c.n4, 1024);
+      if (dense == 0) ew_chan4<OP, 0><<<grid, 256, 0, s>>>(c);
+      else ew_chan4<OP, 1><<<grid, 256, 0, s>>>(c);
+      count_launch();
+      cudaError_t e = cudaGetLastError();
+      *rc = e == cudaSuccess ? PB_OK : cuda_fail(e, "pb_binary");
+      return 1;
+    }
+  }
   if (v4) {
     p.n = (uint32_t)(n / 4);
     p.va = vec[0];
@@ -1536,3 +1660,11 @@ int pb_scale_f32(uint64_t buf, int64_t n, float divisor) {
 }
 
 }  // extern "C"
+
+extern "C" int pb_fastdiv_probe(uint64_t a, uint64_t b, uint64_t out, int64_t n) {
+  if (n <= 0) return PB_OK;
+  fastdiv_probe<<<grid_for(n, 256, 4), 256, 0, compute_stream()>>>((const float*)(uintptr_t)a, (const float*)(uintptr_t)b,
+                                                                    (float*)(uintptr_t)out, n);
+  PB_LAUNCHED();
+  return PB_OK;
+}

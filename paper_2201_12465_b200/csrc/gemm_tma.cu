@@ -326,7 +326,8 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
           mbar_expect_tx(&full[s], C::STAGE);
           const int k0 = kbeg + kb * BK;
           if (!WG) {
-            const int tap = kb / cblocks, c0 = (kb - tap * cblocks) * BK;
+            const int kg = k0 / BK;  // global k-block (split K starts mid-way through the taps)
+            const int tap = kg / cblocks, c0 = (kg - tap * cblocks) * BK;
             const int r = tap / pr.KW, sx = tap - r * pr.KW;
             const int wc = wo * pr.SW - pr.PW, hc = ho * pr.SH - pr.PH;
             if (pr.plain) {  // [rows][K] planes: the k-block is simply k0
@@ -711,11 +712,40 @@ static Prob make_prob(int N, int H, int W, int C, int KH, int KW, int SH, int SW
   return pr;
 }
 
-// D = implicit GEMM over the NHWC planes (xh, xl) and K-major weight planes (wh, wl) [Nj][K]
+static int conv_bn(const Prob& pr) { return pr.Nj <= 64 ? 64 : 128; }  // (128 wins even with a ragged wave)
+
+// split K over z when the tile grid leaves SMs idle (the 14x14 and 7x7 stages at b32: 98 and
+// 52 tiles on 148 SMs): minimise waves x k-blocks per tile plus the partials' round trip
+// (folded in f64, in split order, by fold_partials -- deterministic)
+static int conv_splits(const Prob& pr) {
+  const int64_t tiles = (int64_t)((pr.Mi + BM - 1) / BM) * ((pr.Nj + conv_bn(pr) - 1) / conv_bn(pr));
+  const int64_t nkb = (pr.K + BK - 1) / BK, sms = num_sms();
+  if (tiles >= sms || nkb < 8) return 1;
+  int best = 1;
+  double best_cost = (double)((tiles + sms - 1) / sms) * nkb;
+  for (int sp = 2; sp <= 16 && nkb / sp >= 4; ++sp) {
+    const double cost = (double)((tiles * sp + sms - 1) / sms) * ((nkb + sp - 1) / sp) +
+                        (double)pr.Mi * pr.Nj * sp / 637500.0;  // ~one k-block per 2.5 MB of partials
+    if (cost < best_cost * 0.95) {
+      best = sp;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+static size_t conv_partial_bytes(const Prob& pr) {
+  const int sp = conv_splits(pr);
+  return sp > 1 ? ((size_t)sp * pr.Mi * pr.Nj * 4 + 1023) / 1024 * 1024 : 0;
+}
+
+// D = implicit GEMM over the NHWC planes (xh, xl) and K-major weight planes (wh, wl) [Nj][K];
+// pw: conv_partial_bytes(pr) of scratch for split K (or null: no split)
 template <class OUT>
-static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh, const float* wl, const OUT& o) {
+static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh, const float* wl, const OUT& o,
+                    float* pw = nullptr) {
   CUtensorMap ah, al, bh, bl;
-  const int BN = pr.Nj <= 64 ? 64 : 128;  // (128-wide tiles win even with a ragged last wave)
+  const int BN = conv_bn(pr);
   static int plain_ok = -1;  // experiment hook: PB_TMA_PLAIN=0 keeps 1x1 convs on im2col boxes
   if (plain_ok < 0) {
     const char* e = getenv("PB_TMA_PLAIN");
@@ -729,6 +759,19 @@ static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh,
   if (!ok || !map_2d(&bh, wh, pr.K, pr.Nj, BN) || !map_2d(&bl, wl, pr.K, pr.Nj, BN))
     return fail(PB_ERR_CUDA, "tma conv: tensor map encoding failed");
   pr.zdim = 1;
+  const int sp = pw ? conv_splits(pr) : 1;
+  if (sp > 1) {
+    const int nkb = (pr.K + BK - 1) / BK;
+    pr.kper = (nkb + sp - 1) / sp * BK;
+    pr.zdim = (pr.K + pr.kper - 1) / pr.kper;
+    OutPartial op{pw, pr.Mi, pr.Nj};
+    int rc = BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, op) : launch<128, false>(ah, al, bh, bl, pr, op);
+    if (rc) return rc;
+    fold_partials<OUT><<<grid_for((int64_t)pr.Mi * pr.Nj, 256), 256, 0, compute_stream()>>>(pw, pr.zdim, pr.Mi,
+                                                                                             pr.Nj, o);
+    PB_LAUNCHED();
+    return PB_OK;
+  }
   if (BN == 64) return launch<64, false>(ah, al, bh, bl, pr, o);
   return launch<128, false>(ah, al, bh, bl, pr, o);
 }
@@ -866,16 +909,18 @@ int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias,
   pr.Nj = F;
   pr.K = (int)K;
   const size_t wb = ((size_t)F * K * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
-  char* ws = (char*)workspace(2 * wb + 2 * ab);
+  const size_t pb = conv_partial_bytes(pr);
+  char* ws = (char*)workspace(2 * wb + 2 * ab + pb);
   if (!ws) return fail(PB_ERR_OOM, "conv2d (tma): no workspace");
   float *wh = (float*)ws, *wl = (float*)(ws + wb), *xh = (float*)(ws + 2 * wb), *xl = (float*)(ws + 2 * wb + ab);
+  float* pw = pb ? (float*)(ws + 2 * wb + 2 * ab) : nullptr;
   weight_split<<<grid_for((int64_t)F * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, C, KH, KW, 0, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(C)));
   PB_LAUNCHED();
   int rc = split_act((const float*)(uintptr_t)x->ptr, xh, xl, N, C, H * W);
   if (rc) return rc;
   OutConv o{(float*)(uintptr_t)out->ptr, bias ? (const float*)(uintptr_t)bias->ptr : nullptr, (int)rows, F,
             FastDiv((uint32_t)(pr.HO * pr.WO))};
-  return run_conv(pr, xh, xl, wh, wl, o);
+  return run_conv(pr, xh, xl, wh, wl, o, pw);
 }
 
 // stride-1 dgrad: dx = conv(g, flip(w)^T) with padding KH-1-ph
@@ -960,15 +1005,17 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
   pr.Nj = Cx;
   pr.K = (int)K;
   const size_t wb = ((size_t)Cx * K * 4 + 1023) / 1024 * 1024, ab = ((size_t)act * 4 + 1023) / 1024 * 1024;
-  char* ws = (char*)workspace(2 * wb + 2 * ab);
+  const size_t pb = conv_partial_bytes(pr);
+  char* ws = (char*)workspace(2 * wb + 2 * ab + pb);
   if (!ws) return fail(PB_ERR_OOM, "conv2d_grad_input (tma): no workspace");
   float *wh = (float*)ws, *wl = (float*)(ws + wb), *gh = (float*)(ws + 2 * wb), *gl = (float*)(ws + 2 * wb + ab);
+  float* part = pb ? (float*)(ws + 2 * wb + 2 * ab) : nullptr;
   weight_split<<<grid_for((int64_t)Cx * K, 256), 256, 0, compute_stream()>>>((const float*)(uintptr_t)w->ptr, wh, wl, F, Cx, KH, KW, 1, FastDiv((uint32_t)((KH) * (KW))), FastDiv((uint32_t)(F)));
   PB_LAUNCHED();
   int rc = split_act((const float*)(uintptr_t)gr->ptr, gh, gl, N, F, HO * WO);
   if (rc) return rc;
   OutConv o{(float*)(uintptr_t)out->ptr, nullptr, (int)rows, Cx, FastDiv((uint32_t)(H * W))};
-  return run_conv(pr, gh, gl, wh, wl, o);
+  return run_conv(pr, gh, gl, wh, wl, o, part);
 }
 
 // stride-1 wgrad over the padded output grid (see the header): K = N * ceil(HO*Wp / 32) * 32

@@ -91,6 +91,7 @@ SIGNATURES = {
     "pb_rand": (_I, [_I, _U64, _U64, _B]),
     "pb_rand_dev": (_I, [_I, _U64, _U64, _U64, _B]),
     "pb_counter_add": (_I, [_U64, _U64]),
+    "pb_fastdiv_probe": (_I, [_U64, _U64, _U64, ctypes.c_int64]),
     "pb_reduce": (_I, [_I, _B, _I, _B]),
     "pb_reduce_epi": (_I, [_I, _B, _I, _B, _I, ctypes.c_float, _I]),
     "pb_check": (_I, [_I, _B, _I32P]),

@@ -66,3 +66,20 @@ def compare(name, m, arr, losses, params):
             "sum": rel_err([s for s, _ in sums], [s for s, _ in m["param_sums"]]),
             "abs_sum": rel_err([a for _, a in sums], [a for _, a in m["param_sums"]]),
             "sampled": sampled}
+
+
+def bounds(m):
+    """The bar for one config: losses 1e-3 (north_star), parameter sums 1e-3, sampled
+    parameters 1e-4 -- or twice the reference's own gap under a 1e-7 perturbation of its init
+    where that is larger (ResNet-50's trajectory is chaotic: tests/golden/make_fullsize_golden.py)."""
+    sp = m.get("self_sensitivity_params", {})
+    return {"loss": max(1e-3, 2 * m.get("self_sensitivity", 0.0)),
+            "sum": max(1e-3, 2 * sp.get("sum", 0.0)),
+            "abs_sum": max(1e-3, 2 * sp.get("abs_sum", 0.0)),
+            "sampled": max(1e-4, 2 * sp.get("sampled", 0.0))}
+
+
+def check(err, m):
+    b = bounds(m)
+    for k, v in b.items():
+        assert err[k] <= v, (k, err, b)

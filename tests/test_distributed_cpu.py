@@ -9,6 +9,7 @@ import socket
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 from golden_util import models_meta, rel_err
@@ -50,3 +51,47 @@ def test_two_rank_dp_matches_reference(mode, tmp_path):
 def test_shape_mismatch_raises_on_every_rank(tmp_path):
     res = launch(2, "shape_error", tmp_path)
     assert [r["raised"] for r in res] == ["CollectiveShapeError"] * 2
+
+
+def dp_meta():
+    with open(os.path.join(HERE, "golden", "dp.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("mode", ["acceptance_sync", "acceptance_bucketed"])
+def test_reference_dp_acceptance_fixture(mode, tmp_path):
+    """The reference's own DP acceptance fixture (T/test_acceptance.py:394-440) on 4 process
+    ranks: every rank's 50 losses equal the reference's thread-rank run (tests/golden/dp.json,
+    made by make_dp_golden.py), the rank mean stays within 1e-3 of the single-rank run, and
+    the metadata checks leave a bounded number of keys in the store."""
+    gold = dp_meta()["acceptance"]
+    res = launch(4, mode, tmp_path)
+    for r in range(4):
+        assert rel_err(res[r]["losses"], gold["ranks"][r]) <= 1e-5, r
+    assert rel_err(res[0]["param_sums"], gold["param_sums"]) <= 1e-5
+    assert all(res[r]["param_sums"] == res[0]["param_sums"] for r in range(4))
+    gap = max(abs(float(np.mean([res[r]["losses"][k] for r in range(4)])) - gold["single"][k])
+              for k in range(gold["steps"]))
+    assert gap <= 1e-3, gap
+    if mode == "acceptance_sync":  # 50 per-step checks, at most two checks' keys live per rank
+        assert res[0]["store_keys"] <= 4 * 2 + 8, res[0]["store_keys"]
+
+
+def test_batchnorm_dp_matches_reference_thread_ranks(tmp_path):
+    """BatchNorm statistics stay per rank; a 2-rank ResNet run equals the
+    reference's run_ranks on the same shards (losses, parameters, running statistics)."""
+    gold = dp_meta()["bn"]
+    res = launch(2, "bn", tmp_path)
+    for r in range(2):
+        assert rel_err(res[r]["losses"], gold["ranks"][r]) <= 1e-5, (r, res[r]["losses"], gold["ranks"][r])
+        assert rel_err(res[r]["buffer_sums"], gold["buffer_sums"][r]) <= 1e-5
+    assert rel_err(res[0]["param_sums"], gold["param_sums"][0]) <= 1e-4
+    assert res[0]["buffer_sums"] != res[1]["buffer_sums"]  # per-rank statistics differ
+
+
+def test_broadcast_accepts_none_and_any_placeholder_off_root(tmp_path):
+    """minml's broadcast contract (test_broadcast_accepts_none_off_root): only the root's
+    tensor matters; other ranks may pass None or a placeholder of another shape."""
+    res = launch(2, "broadcast", tmp_path)
+    want = (np.arange(6, dtype=np.float32).reshape(2, 3) + 10).tolist()
+    assert all(r["a"] == want and r["b"] == want for r in res)

@@ -8,8 +8,14 @@ Tolerances, all under the reference's metric |a-b|/max(|a|,|b|,1)
 (T/test_acceptance.py:260-262):
   * losses: 1e-3 over the 10 steps (BASELINE.json north_star);
   * every parameter's signed sum and sum|p|: 1e-3;
-  * 64 sampled elements of every parameter: 1e-4.
-The measured errors are written to gpurun_out/fullsize_parity.jsonl."""
+  * 64 sampled elements of every parameter: 1e-4;
+  * except where the reference's own trajectory moves more than that under a 1e-7
+    perturbation of its init (ResNet-50): then twice that self-sensitivity
+    (fullsize_util.bounds).
+The measured errors are written to gpurun_out/fullsize_parity.jsonl beside the reference's
+own conditioning (``self_sensitivity``: its 10-step loss gap when the init is perturbed by
+1e-7, i.e. by about one f32 ulp; ResNet-50 at batch 2 trains at lr 1e-5 to keep that well
+below the 1e-3 bar -- see make_fullsize_golden.py)."""
 
 import json
 import os
@@ -17,7 +23,7 @@ import os
 import numpy as np
 import pytest
 
-from fullsize_util import BUILDERS, arrays, compare, meta, run
+from fullsize_util import BUILDERS, arrays, bounds, check, compare, meta, run
 from gpu_util import gpu_backend
 
 pytestmark = pytest.mark.gpu
@@ -36,8 +42,8 @@ def test_fullsize_config_matches_reference(name, mode):
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, "fullsize_parity.jsonl"), "a") as f:
         f.write(json.dumps({"config": name, "mode": mode, "batch": m["batch"], "errors": err,
-                            "losses": losses, "ref_losses": m["losses"]}) + "\n")
-    assert err["loss"] <= 1e-3, (err, losses, m["losses"])
-    assert err["sum"] <= 1e-3 and err["abs_sum"] <= 1e-3, err
-    assert err["sampled"] <= 1e-4, err
+                            "ref_self_sensitivity": m.get("self_sensitivity"), "bounds": bounds(m),
+                            "losses": losses,
+                            "ref_losses": m["losses"]}) + "\n")
+    check(err, m)
     assert all(np.isfinite(p).all() for p in params)

@@ -8,7 +8,7 @@ the reference's metric) for transcendental ops, reductions and contractions."""
 import numpy as np
 import pytest
 
-from golden_util import check_against, contraction_err, op_cases, rel_err
+from golden_util import assert_contraction, check_against, f32_conv_family, op_cases, rel_err
 from gpu_util import gpu_backend
 from paper_2201_12465_b200 import _tensor as T
 from paper_2201_12465_b200 import errors
@@ -145,7 +145,7 @@ def test_matmul_sizes(gpu, m, k, n):
     b = r.standard_normal((k, n)).astype(np.float32) / np.sqrt(k)
     got = (T.tensor(a, backend=gpu.name) @ T.tensor(b, backend=gpu.name)).to_host_buffer()
     want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
-    assert contraction_err(got, want) <= 1e-5
+    assert_contraction(got, want, lambda: a @ b)
 
 
 CONV = [((32, 64, 56, 56), (64, 64, 3, 3), 1, 1), ((8, 256, 56, 56), (128, 256, 1, 1), 2, 0),
@@ -160,13 +160,22 @@ def test_conv_sizes(gpu, xs, ws, s, p):
     params = {"stride": (s, s), "padding": (p, p)}
     tx, tw = T.tensor(x, backend=gpu.name), T.tensor(w, backend=gpu.name)
     out = T.conv2d(tx, tw, None, s, p)
-    assert rel_err(out.to_host_buffer(), _oracle("conv2d", params, [x, w])) <= 1e-5
+    assert_contraction(out.to_host_buffer(), _oracle("conv2d", params, [x, w]),
+                       lambda: f32_conv_family(x, w, None, s, p)[0], what="fprop")
     g = r.standard_normal(tuple(out.shape)).astype(np.float32)
     tg = T.tensor(g, backend=gpu.name)
+    fam = {}
+
+    def blas(i):
+        if "v" not in fam:
+            fam["v"] = f32_conv_family(x, w, g, s, p)
+        return fam["v"][i]
     gi = T.conv2d_grad_input(tg, tw, xs, s, p).to_host_buffer()
-    assert rel_err(gi, _oracle("conv2d_grad_input", dict(params, x_shape=xs), [g, w])) <= 1e-5
+    assert_contraction(gi, _oracle("conv2d_grad_input", dict(params, x_shape=xs), [g, w]), lambda: blas(1),
+                       what="dgrad")
     gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()  # reduces over N*Ho*Wo (up to 100352)
-    assert contraction_err(gw, _oracle("conv2d_grad_weight", dict(params, w_shape=ws), [x, g])) <= 1e-5
+    assert_contraction(gw, _oracle("conv2d_grad_weight", dict(params, w_shape=ws), [x, g]), lambda: blas(2),
+                       what="wgrad")
 
 
 def test_times_one_is_a_broadcast_view(gpu):
@@ -189,3 +198,45 @@ def test_times_one_is_a_broadcast_view(gpu):
     # anything but an exact f32 one keeps the multiply
     twos = T.full((2, 3, 14, 5), 2.0, dtype="f32", backend=gpu.name)
     assert (twos * tg).adapter.block is not tg.adapter.block
+
+
+def test_fast_division_is_ieee_exact(gpu):
+    """The per-row broadcast kernel divides by reciprocal + one exact-residual correction
+    (csrc/elementwise.cu div_rn_rcp); it must equal IEEE division bit for bit: 2^26 random
+    bit patterns, every mantissa of the divisor against 8 dividends, and the edge exponents."""
+    r = np.random.default_rng(11)
+    n = 1 << 26
+    a = r.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    b = r.integers(0, 2 ** 32, n, dtype=np.uint64).astype(np.uint32).view(np.float32)
+    mant = (np.arange(1 << 23, dtype=np.uint32) | np.uint32(127 << 23)).view(np.float32)
+    for dividend in (1.0, 1.5, 1.9999999, 3.0, 1.0000001, 1.2345678, 7.654321e-30, 6.5e35):
+        a = np.concatenate([a, np.full(mant.size, dividend, np.float32)])
+        b = np.concatenate([b, mant])
+    edge = np.array([2.0 ** e for e in range(-149, 128)] + [np.inf, -np.inf, np.nan, 0.0, -0.0], np.float32)
+    ea, eb = np.meshgrid(edge, edge * np.float32(1.0000001))
+    a = np.concatenate([a, ea.ravel(), edge])
+    b = np.concatenate([b, eb.ravel(), np.float32(3.0) * edge])
+    with np.errstate(all="ignore"):
+        want = a / b
+    ta, tb = T.tensor(a, backend=gpu.name), T.tensor(b, backend=gpu.name)
+    out = T.tensor(np.zeros_like(a), backend=gpu.name)
+    gpu._lib.pb_fastdiv_probe(ta.adapter.ptr, tb.adapter.ptr, out.adapter.ptr, a.size)
+    got = out.numpy()
+    bad = ~((got.view(np.uint32) == want.view(np.uint32)) | (np.isnan(got) & np.isnan(want)))
+    assert not bad.any(), (int(bad.sum()), a[bad][:5], b[bad][:5], got[bad][:5], want[bad][:5])
+
+
+@pytest.mark.parametrize("op", ["add", "sub", "mul", "div"])
+@pytest.mark.parametrize("left", [False, True])
+def test_row_broadcast_kernel_bit_exact(gpu, op, left):
+    """BatchNorm's [N,C,H,W] (op) [1,C,1,1] shapes, either side: the per-row kernel
+    (ew_chan4) against numpy's f32 arithmetic, bit for bit."""
+    r = np.random.default_rng(5)
+    x = r.standard_normal((4, 64, 28, 28)).astype(np.float32)
+    m = (r.standard_normal((1, 64, 1, 1)) + 3).astype(np.float32)
+    tx, tm = T.tensor(x, backend=gpu.name), T.tensor(m, backend=gpu.name)
+    f = {"add": lambda u, v: u + v, "sub": lambda u, v: u - v, "mul": lambda u, v: u * v,
+         "div": lambda u, v: u / v}[op]
+    got = (f(tm, tx) if left else f(tx, tm)).numpy()
+    want = f(m, x) if left else f(x, m)
+    assert got.dtype == np.float32 and np.array_equal(got, want)

@@ -4,14 +4,15 @@ rounds once), on every code path the dispatcher can take: row-/k-mode operand lo
 vectorised and scalar gathers, strided convs, stride-2 dgrad, split-K wgrad and matmul,
 batched matmul, transposed views, ragged tiles.
 
-Tolerance: 1e-5 under the contraction metric |a-b|/max(|a|,|b|,1,rms(ref)) of
-tests/golden_util.py (the reference's metric, with the output rms added to the floor: an f32
-accumulation's absolute error scales with the terms summed, not with the cancelled result)."""
+Tolerance: the reference's metric |a-b|/max(|a|,|b|,1) <= 1e-5 (T/test_acceptance.py:260-262),
+through golden_util.assert_contraction: where a long K-reduction of O(1) terms cancels below
+what any f32-accumulating GEMM resolves, the kernel must instead beat numpy's own f32 BLAS on
+the same operands by 2x under that metric (see its docstring)."""
 
 import numpy as np
 import pytest
 
-from golden_util import contraction_err as rel_err
+from golden_util import assert_contraction, contraction_err, f32_conv_family
 from gpu_util import gpu_backend
 from paper_2201_12465_b200 import _tensor as T
 
@@ -84,16 +85,19 @@ def test_conv_family_tc(gpu, path, xs, ws, s, p):
     tx, tw, tb = (T.tensor(a, backend=gpu.name) for a in (x, w, b))
     want, cols = _np_conv(x, w, s, p)
     got = T.conv2d(tx, tw, tb, s, p).to_host_buffer()
-    assert rel_err(got, (want + b[None, :, None, None]).astype(np.float32)) <= TOL
+    y32 = lambda: f32_conv_family(x, w, None, s, p)[0]  # noqa: E731
+    assert_contraction(got, (want + b[None, :, None, None]).astype(np.float32),
+                       lambda: y32() + b[None, :, None, None], what="fprop+bias")
     got_nb = T.conv2d(tx, tw, None, s, p).to_host_buffer()
-    assert rel_err(got_nb, want.astype(np.float32)) <= TOL
+    assert_contraction(got_nb, want.astype(np.float32), y32, what="fprop")
     g = r.standard_normal(got.shape).astype(np.float32)
     tg = T.tensor(g, backend=gpu.name)
     gi = T.conv2d_grad_input(tg, tw, xs, s, p).to_host_buffer()
-    assert rel_err(gi, _np_dgrad(g, w, xs, s, p).astype(np.float32)) <= TOL
+    assert_contraction(gi, _np_dgrad(g, w, xs, s, p).astype(np.float32),
+                       lambda: f32_conv_family(x, w, g, s, p)[1], what="dgrad")
     gw = T.conv2d_grad_weight(tx, tg, ws, s, p).to_host_buffer()
     want_w = np.einsum("ncrshw,nfhw->fcrs", cols, g.astype(np.float64))
-    assert rel_err(gw, want_w.astype(np.float32)) <= TOL
+    assert_contraction(gw, want_w.astype(np.float32), lambda: f32_conv_family(x, w, g, s, p)[2], what="wgrad")
 
 
 MATMULS = [(64, 784, 256), (64, 256, 10), (256, 64, 10), (784, 64, 256), (1000, 17, 3), (1, 1, 1),
@@ -107,13 +111,14 @@ def test_matmul_layouts_tc(gpu, m, k, n):
     b = (r.standard_normal((k, n)) / np.sqrt(k)).astype(np.float32)
     want = (a.astype(np.float64) @ b.astype(np.float64)).astype(np.float32)
     ta, tb = T.tensor(a, backend=gpu.name), T.tensor(b, backend=gpu.name)
-    assert rel_err((ta @ tb).to_host_buffer(), want) <= TOL
+    blas = lambda: a @ b  # noqa: E731
+    assert_contraction((ta @ tb).to_host_buffer(), want, blas)
     # transposed views for both operands (Linear's W^T and matmul backward): no copies
     at = T.tensor(np.ascontiguousarray(a.T), backend=gpu.name).transpose()
     bt = T.tensor(np.ascontiguousarray(b.T), backend=gpu.name).transpose()
-    assert rel_err((at @ tb).to_host_buffer(), want) <= TOL
-    assert rel_err((ta @ bt).to_host_buffer(), want) <= TOL
-    assert rel_err((at @ bt).to_host_buffer(), want) <= TOL
+    assert_contraction((at @ tb).to_host_buffer(), want, blas)
+    assert_contraction((ta @ bt).to_host_buffer(), want, blas)
+    assert_contraction((at @ bt).to_host_buffer(), want, blas)
 
 
 def test_batched_matmul_tc(gpu):
@@ -122,14 +127,16 @@ def test_batched_matmul_tc(gpu):
     b = r.standard_normal((6, 64, 100)).astype(np.float32) / 8
     want = np.einsum("bmk,bkn->bmn", a.astype(np.float64), b.astype(np.float64)).astype(np.float32)
     ta, tb = T.tensor(a, backend=gpu.name), T.tensor(b, backend=gpu.name)
-    assert rel_err((ta @ tb).to_host_buffer(), want) <= TOL
+    assert_contraction((ta @ tb).to_host_buffer(), want, lambda: np.matmul(a, b))
     # attention-style transposed operand: b^T stored as [6,100,64]
     bt = T.tensor(np.ascontiguousarray(np.transpose(b, (0, 2, 1))), backend=gpu.name).transpose((0, 2, 1))
-    assert rel_err((ta @ bt).to_host_buffer(), want) <= TOL
+    assert_contraction((ta @ bt).to_host_buffer(), want, lambda: np.matmul(a, b))
 
 
 def test_tc_matches_simt_path(gpu):
-    """The SIMT kernels (f64 accumulation) are the in-library reference for the tc path."""
+    """The SIMT kernels (f64 accumulation) are the in-library reference for the tc path: the
+    tcgen05 families agree with them to 1e-5 of the output scale (all-ones gradients make the
+    wgrad sums cancel-free, so this is the plain relative agreement of the two families)."""
     r = np.random.default_rng(4)
     x = r.standard_normal((4, 64, 28, 28)).astype(np.float32)
     w = (r.standard_normal((128, 64, 3, 3)) / 24).astype(np.float32)
@@ -150,7 +157,7 @@ def test_tc_matches_simt_path(gpu):
     for other in (outs[n:2 * n], outs[2 * n:]):
         for a, b in zip(outs[:n], other):
             for u, v in zip(a, b):
-                assert rel_err(u, v) <= TOL
+                assert contraction_err(u, v) <= TOL
 
 
 @pytest.mark.parametrize("m,k,n", [(256, 96, 80), (300, 770, 130), (2048, 768, 64), (256, 2048, 96), (512, 67, 257)])
@@ -169,15 +176,16 @@ def test_tma_matmul_matches_f64_reference(gpu, m, k, n):
     got = T.matmul(ta, tw.transpose()).to_host_buffer()              # W^T as a strided view
     assert gpu.launch_count() - launches0 >= 3                         # 2 pre-passes + the GEMM
     want = (a.astype(np.float64) @ w.astype(np.float64).T).astype(np.float32)
-    assert rel_err(got, want) <= TOL
+    assert_contraction(got, want, lambda: a @ w.T, what="x @ W^T")
     g = r.standard_normal((m, n)).astype(np.float32)
     tg = T.tensor(g, backend=gpu.name)
     got = T.matmul(tg, tw).to_host_buffer()                            # [m,n] x [n,k]
-    assert rel_err(got, (g.astype(np.float64) @ w.astype(np.float64)).astype(np.float32)) <= TOL
+    assert_contraction(got, (g.astype(np.float64) @ w.astype(np.float64)).astype(np.float32), lambda: g @ w,
+                       what="g @ W")
     if k >= 256:
         got = T.matmul(tg.transpose(), ta).to_host_buffer()           # [n,m] x [m,k], M = n
         want = (g.astype(np.float64).T @ a.astype(np.float64)).astype(np.float32)
-        assert rel_err(got, want) <= TOL
+        assert_contraction(got, want, lambda: g.T @ a, what="g^T @ x")
 
 
 @pytest.mark.parametrize("n,c,h,f,s", [(8, 64, 14, 128, 1), (4, 96, 20, 64, 2), (8, 128, 14, 256, 1), (2, 256, 28, 64, 2),
@@ -194,7 +202,8 @@ def test_wgrad_1x1_gemm_matches_f64_reference(gpu, n, c, h, f, s):
     got = T.conv2d_grad_weight(tx, tg, (f, c, 1, 1), s, 0).to_host_buffer()
     xs = x[:, :, ::s, ::s].astype(np.float64)
     want = np.einsum("nfhw,nchw->fc", g.astype(np.float64), xs).astype(np.float32)[:, :, None, None]
-    assert rel_err(got, want) <= TOL
+    blas = lambda: np.tensordot(g, xs.astype(np.float32), axes=([0, 2, 3], [0, 2, 3]))[:, :, None, None]  # noqa: E731
+    assert_contraction(got, want, blas, what="1x1 wgrad")
 
 
 def _np_dgrad(g, w, xshape, s, p):
@@ -222,4 +231,5 @@ def test_subpixel_dgrad_matches_f64_reference(gpu, n, c, h, f, k, s, p):
     w = (r.standard_normal((f, c, k, k)) / np.sqrt(f * k * k)).astype(np.float32)
     got = T.conv2d_grad_input(T.tensor(g, backend=gpu.name), T.tensor(w, backend=gpu.name), (n, c, h, h), s,
                               p).to_host_buffer()
-    assert rel_err(got, _np_dgrad(g, w, (n, c, h, h), s, p)) <= TOL
+    assert_contraction(got, _np_dgrad(g, w, (n, c, h, h), s, p),
+                       lambda: f32_conv_family(np.zeros((n, c, h, h), np.float32), w, g, s, p)[1], what="dgrad")
