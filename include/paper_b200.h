@@ -155,6 +155,23 @@ typedef struct pb_chain_step {
 } pb_chain_step;
 int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
                 const pb_chain_step* steps, const pb_tensor* out);
+/* Fused multi-stage f32 sum over an elementwise chain (minml/nn.py:288-306
+ * BatchNorm's x.mean(3).mean(2).mean(0) and minml/autograd.py:290-297 _unbroadcast's
+ * sum(0).sum(2).sum(3)): the source is the chain above evaluated over src_shape (a plain tensor
+ * is one leaf and no steps); stage k sums source axis stages[k].axis (f64 accumulation, one f32
+ * rounding) and applies its optional scalar epilogue, as pb_reduce_epi would.  out: dense f32
+ * holding the kept axes in order.  Supported (else PB_ERR_UNSUPPORTED, nothing launched): 2-3
+ * stages whose first two are (innermost, next) -- "rows" -- or 3 stages whose last is the
+ * innermost axis -- "cols". */
+typedef struct pb_red_stage {
+  int32_t axis;     /* source axis */
+  int32_t epi_op;   /* -1 none, else PB_ADD/SUB/MUL/DIV */
+  int32_t epi_left; /* scalar on the left */
+  float scalar;
+} pb_red_stage;
+int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                    const pb_chain_step* steps, int src_ndim, const int64_t* src_shape, int nstages,
+                    const pb_red_stage* stages, const pb_tensor* out);
 /* In-place multi-tensor SGD (minml/optim.py:64-72 op for op): for each i,
  * g' = g + wd*p (if wd); v = v*mu + g' (if mu, else v := g'); p = p - v*lr.  f32 only. */
 int pb_sgd(int n, const uint64_t* params_in, const uint64_t* params_out, const uint64_t* grads,

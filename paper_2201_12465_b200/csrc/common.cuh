@@ -35,6 +35,9 @@ int num_sms();
 void count_launch();
 // grow-only device scratch on the compute stream (stream order makes reuse safe)
 void* workspace(size_t bytes);
+// n zeroed ticket counters (nullptr if n > kTickCounters); users leave them zero again
+constexpr int64_t kTickCounters = 1 << 16;
+unsigned* tick_counters(int64_t n);
 
 // ---- dtypes -------------------------------------------------------------------------
 inline int itemsize(int dt) {

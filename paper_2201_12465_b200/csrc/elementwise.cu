@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <vector>
 #include <cstring>
+#include <cstdlib>
 #include "common.cuh"
 
 namespace pb {
@@ -64,6 +65,40 @@ PB_BIN(PB_GT, bool, a > b)
 PB_BIN(PB_AND, bool, (bool)a && (bool)b)
 PB_BIN(PB_OR, bool, (bool)a || (bool)b)
 #undef PB_BIN
+
+// a / b correctly rounded, given r = RN(1/b) (Markstein: q = RN(a*r) is within one ulp of
+// a/b, the residual a - q*b is exact with one FMA, and RN(q + residual*r) is RN(a/b)).  The
+// theorem needs every intermediate normal: operands outside [2^-60, 2^60] (zeros, subnormals,
+// inf, NaN included) take the IEEE division instead.  Checked bit for bit against IEEE
+// division in tests/test_gpu_ops.py::test_fast_division_is_ieee_exact.
+__device__ __forceinline__ float div_rn_rcp(float a, float b, float r) {
+  const float aa = fabsf(a), ab = fabsf(b);
+  if (ab >= 0x1p-60f && ab <= 0x1p60f) {
+    if (aa >= 0x1p-60f && aa <= 0x1p60f) {
+      const float q = __fmul_rn(a, r);
+      const float e = __fmaf_rn(-q, b, a);
+      return __fmaf_rn(e, r, q);
+    }
+    if (a == 0.f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & (int)0x80000000);
+  }
+  return a / b;
+}
+
+// IEEE a / b for every input: a normal-range divisor takes its IEEE reciprocal and div_rn_rcp (a
+// zero dividend gives the signed zero directly), anything else the hardware division.  The
+// hardware sequence's fast-path check (FCHK) sends zero dividends -- half of a ReLU-masked
+// gradient -- to its slow subroutine; this path never calls it for them.
+__device__ __forceinline__ float div_ieee(float a, float b) {
+  const float ab = fabsf(b);
+  if (ab >= 0x1p-60f && ab <= 0x1p60f) return div_rn_rcp(a, b, __frcp_rn(b));
+  return a / b;
+}
+
+template <>
+struct Bin<PB_DIV, float> {
+  typedef float res;
+  __device__ __forceinline__ static float f(float a, float b) { return div_ieee(a, b); }
+};
 
 template <typename T> __device__ __forceinline__ T neg_(T v) { return (T)(-v); }
 template <> __device__ __forceinline__ bool neg_(bool v) { return v; }
@@ -350,21 +385,6 @@ struct ChanArgs {
   uint32_t rs[3];     // R's element strides along them
 };
 
-// a / b correctly rounded, given r = RN(1/b) (Markstein: q = RN(a*r) is within one ulp of
-// a/b, the residual a - q*b is exact with one FMA, and RN(q + residual*r) is RN(a/b)).  The
-// theorem needs every intermediate normal: operands outside [2^-60, 2^60] (zeros, subnormals,
-// inf, NaN included) take the IEEE division instead.  Checked bit for bit against IEEE
-// division in tests/test_gpu_ops.py::test_fast_division_is_ieee_exact.
-__device__ __forceinline__ float div_rn_rcp(float a, float b, float r) {
-  const float aa = fabsf(a), ab = fabsf(b);
-  if (aa >= 0x1p-60f && aa <= 0x1p60f && ab >= 0x1p-60f && ab <= 0x1p60f) {
-    const float q = __fmul_rn(a, r);
-    const float e = __fmaf_rn(-q, b, a);
-    return __fmaf_rn(e, r, q);
-  }
-  return a / b;
-}
-
 template <int OP, int RLEFT>
 __global__ void __launch_bounds__(256) ew_chan4(ChanArgs p) {
   typedef typename Bin<OP, float>::res R;
@@ -414,10 +434,10 @@ __global__ void __launch_bounds__(256) ew_chan4(ChanArgs p) {
   }
 }
 
-// exact-division probe for the tests: out[i] = div_rn_rcp(a[i], b[i], RN(1/b[i]))
+// exact-division probe for the tests: out[i] = div_ieee(a[i], b[i]) (div_rn_rcp behind it)
 __global__ void fastdiv_probe(const float* a, const float* b, float* out, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = div_rn_rcp(a[i], b[i], __frcp_rn(b[i]));
+    out[i] = div_ieee(a[i], b[i]);
 }
 
 // ------------------------------------------------------------- fused elementwise chains
@@ -1298,6 +1318,448 @@ __global__ void scale_kernel(float* buf, int64_t n, float div) {
     buf[i] = __fdiv_rn(buf[i], div);
 }
 
+
+// ------------------------------------------------------- fused multi-stage reductions
+// The reference composes per-channel statistics from single-axis f32 sums, each rounded to
+// f32 and usually followed by a scalar op: BatchNorm's batch mean is
+// x.mean(3).mean(2).mean(0) (minml/nn.py:288-306, mean = sum / n, minml/ops.py:33-36) and
+// _unbroadcast reduces a [N, C, H, W] gradient to [1, C, 1, 1] with sum(0).sum(2).sum(3)
+// (minml/autograd.py:290-297), usually of a product such as g * xhat.  pb_reduce_chain runs
+// such a chain -- source elementwise chain, 2-3 sum stages, their scalar epilogues -- in one
+// launch with the same arithmetic per stage: f32 terms summed in f64, rounded to f32, then the
+// epilogue in f32.  Only the order of the f64 additions differs from the one-kernel-per-stage
+// path, which changes the rounded f32 result only when a partial-sum rounding in f64 (2^-53)
+// straddles an f32 rounding boundary.
+//   rows mode  stage 1 over the innermost axis (w), stage 2 over h, stage 3 over an outer axis:
+//              a sub-warp per row, lanes interleaved (float4 per lane when the rows allow),
+//              butterfly fold; stage 2 by one thread per i3 in row order.
+//   cols mode  stage 1 over an outer axis (n), stage 3 over the innermost axis (w): a thread
+//              per (h, 4 consecutive w) walks n in order with 16-byte loads.
+// A block owns one output group (kept index) and a range of stage-3 indices; with several
+// blocks per group the stage-2 values go to a workspace and the group's last block (ticket)
+// sums them in index order.
+struct RCArgs {
+  const void* leaf[kChainLeaves];
+  int8_t is_bool[kChainLeaves];
+  int8_t s_vec[kChainLeaves];  // V4: unit stride along the vector axis (else broadcast)
+  int nleaves, nsteps, head_kind;
+  float head_scalar;
+  ChainStep step[kChainSteps];
+  int64_t s1[kChainLeaves], s2[kChainLeaves], s3[kChainLeaves];  // leaf strides along the stage axes
+  int64_t ks[kChainLeaves][3];                                     // ... along the kept axes (outer first)
+  FastDiv kd1, kd2;                                                // kept extents 1 and 2 (group decode)
+  int E1, E2, E3, nst;
+  int epi[3], epil[3];
+  float epis[3];
+  int r3, nsplit;
+  int U1, pp, E1p;  // rows: units per row (E1 / 4 or E1), planes per pass, padded smem row pitch
+  FastDiv fU1, fE2;
+  int P, S;         // cols: pairs per pass, slices of the stage-1 axis
+  float* out;
+  float* ws;
+  unsigned* tick;
+};
+
+// B source values -- float4s along the vector axis (V4) or scalars in .x -- with one dispatch per
+// chain step for all of them (the interpreter's switch is paid once per B x 4 elements, and the
+// kernel holds one copy of it).  The host admits only the steps handled here (no transcendental
+// ops), so a step is the same Bin/Un functor the unfused kernels apply: bit-identical values.
+template <int NL, int B, bool V4>
+__device__ __forceinline__ void rc_eval_batch(const RCArgs& p, const int64_t (&off)[B][NL], const bool (&on)[B],
+                                              float4 (&v)[B]) {
+  float4 x[NL][B];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const bool vec = V4 && p.s_vec[l];
+    if (p.is_bool[l]) {
+      const uint8_t* b8 = (const uint8_t*)p.leaf[l];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (!on[u]) continue;
+        if (vec) {
+          const uchar4 c = *reinterpret_cast<const uchar4*>(b8 + off[u][l]);
+          x[l][u] = make_float4(c.x ? 1.f : 0.f, c.y ? 1.f : 0.f, c.z ? 1.f : 0.f, c.w ? 1.f : 0.f);
+        } else {
+          const float t = b8[off[u][l]] ? 1.f : 0.f;
+          x[l][u] = make_float4(t, t, t, t);
+        }
+      }
+    } else {
+      const float* f = (const float*)p.leaf[l];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        if (!on[u]) continue;
+        if (vec) {
+          x[l][u] = __ldg(reinterpret_cast<const float4*>(f + off[u][l]));
+        } else {
+          const float t = __ldg(f + off[u][l]);
+          x[l][u] = make_float4(t, t, t, t);
+        }
+      }
+    }
+  }
+  const float4 hs = make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
+#pragma unroll
+  for (int u = 0; u < B; ++u) v[u] = p.head_kind == 0 ? x[0][u] : hs;
+  for (int s = 0; s < p.nsteps; ++s) {
+    const ChainStep st = p.step[s];
+    float4 o[B];
+    if (st.kind == 1) {
+      const int sl = st.leaf;
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        float4 t = x[0][u];
+        if constexpr (NL > 1) t = sl == 1 ? x[NL > 1 ? 1 : 0][u] : t;
+        if constexpr (NL > 2) t = sl == 2 ? x[NL > 2 ? 2 : 0][u] : t;
+        if constexpr (NL > 3) t = sl == 3 ? x[NL > 3 ? 3 : 0][u] : t;
+        if constexpr (NL > 4) t = sl == 4 ? x[NL > 4 ? 4 : 0][u] : t;
+        if constexpr (NL > 5) t = sl == 5 ? x[NL > 5 ? 5 : 0][u] : t;
+        if constexpr (NL > 6) t = sl == 6 ? x[NL > 6 ? 6 : 0][u] : t;
+        if constexpr (NL > 7) t = sl == 7 ? x[NL > 7 ? 7 : 0][u] : t;
+        o[u] = t;
+      }
+    } else if (st.kind == 2) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) o[u] = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
+    } else {
+#pragma unroll
+      for (int u = 0; u < B; ++u) o[u] = v[u];
+    }
+    if (st.kind != 0 && st.side) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const float4 t = v[u];
+        v[u] = o[u];
+        o[u] = t;
+      }
+    }
+#define RC_LANES(...)                                  \
+  _Pragma("unroll") for (int u = 0; u < B; ++u) {     \
+    float a_, b_;                                      \
+    a_ = v[u].x; b_ = o[u].x; v[u].x = (__VA_ARGS__);  \
+    a_ = v[u].y; b_ = o[u].y; v[u].y = (__VA_ARGS__);  \
+    a_ = v[u].z; b_ = o[u].z; v[u].z = (__VA_ARGS__);  \
+    a_ = v[u].w; b_ = o[u].w; v[u].w = (__VA_ARGS__);  \
+    (void)b_;                                          \
+  }
+    if (st.kind == 0) {
+      switch (st.op - 64) {
+        case PB_NEG: RC_LANES(Un<PB_NEG, float>::f(a_)) break;
+        case PB_ABS: RC_LANES(Un<PB_ABS, float>::f(a_)) break;
+        case PB_NOT: RC_LANES(a_ == 0.f ? 1.f : 0.f) break;
+        default:
+          if (st.to_bool) RC_LANES(a_ != 0.f ? 1.f : 0.f)
+          break;
+      }
+      continue;
+    }
+    switch (st.op) {
+      case PB_ADD: RC_LANES(Bin<PB_ADD, float>::f(a_, b_)) break;
+      case PB_SUB: RC_LANES(Bin<PB_SUB, float>::f(a_, b_)) break;
+      case PB_MUL: RC_LANES(Bin<PB_MUL, float>::f(a_, b_)) break;
+      case PB_DIV: RC_LANES(Bin<PB_DIV, float>::f(a_, b_)) break;
+      case PB_MIN: RC_LANES(Bin<PB_MIN, float>::f(a_, b_)) break;
+      case PB_MAX: RC_LANES(Bin<PB_MAX, float>::f(a_, b_)) break;
+      case PB_EQ: RC_LANES(a_ == b_ ? 1.f : 0.f) break;
+      case PB_LT: RC_LANES(a_ < b_ ? 1.f : 0.f) break;
+      case PB_GT: RC_LANES(a_ > b_ ? 1.f : 0.f) break;
+      case PB_AND: RC_LANES((a_ != 0.f && b_ != 0.f) ? 1.f : 0.f) break;
+      default: RC_LANES((a_ != 0.f || b_ != 0.f) ? 1.f : 0.f) break;
+    }
+#undef RC_LANES
+  }
+}
+
+// plain source (one dense f32 leaf, no steps)
+template <int B, bool V4>
+__device__ __forceinline__ void rc_load_batch(const RCArgs& p, const int64_t (&off)[B][1], const bool (&on)[B],
+                                              float4 (&v)[B]) {
+  const float* f = (const float*)p.leaf[0];
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    if (!on[u]) continue;
+    if (V4) {
+      v[u] = __ldg(reinterpret_cast<const float4*>(f + off[u][0]));
+    } else {
+      const float t = __ldg(f + off[u][0]);
+      v[u] = make_float4(t, t, t, t);
+    }
+  }
+}
+
+template <int NL, int B, bool V4, bool PLAIN>
+__device__ __forceinline__ void rc_source(const RCArgs& p, const int64_t (&off)[B][NL], const bool (&on)[B],
+                                          float4 (&v)[B]) {
+  if constexpr (PLAIN) rc_load_batch<B, V4>(p, off, on, v);
+  else rc_eval_batch<NL, B, V4>(p, off, on, v);
+}
+
+__device__ __forceinline__ float rc_epi(const RCArgs& p, int k, float v) {
+  const int op = p.epi[k];
+  if (op < 0) return v;
+  const float a = p.epil[k] ? p.epis[k] : v, b = p.epil[k] ? v : p.epis[k];
+  switch (op) {
+    case PB_ADD: return a + b;
+    case PB_SUB: return a - b;
+    case PB_MUL: return a * b;
+    default: return a / b;
+  }
+}
+
+template <int NL>
+__device__ __forceinline__ void rc_group_base(const RCArgs& p, int g, int64_t (&gb)[NL]) {
+  uint32_t t, k0, k1, k2;
+  p.kd2.divmod((uint32_t)g, t, k2);
+  p.kd1.divmod(t, k0, k1);
+#pragma unroll
+  for (int l = 0; l < NL; ++l) gb[l] = (int64_t)k0 * p.ks[l][0] + (int64_t)k1 * p.ks[l][1] + (int64_t)k2 * p.ks[l][2];
+}
+
+// rows mode: block (group g, planes [i3a, i3a + np)) evaluates its planes (E2 rows x E1, contiguous
+// for dense sources) into shared memory -- several units per thread in flight, 16-byte loads when
+// rows allow -- then a thread per row sums it in f64 (4 chains) from the odd-pitch (conflict-free)
+// buffer, a warp per plane folds the rows (stage 2), and stage 3 folds the planes: in the block when
+// it holds them all, else through the workspace in the group's last block (ticket)
+template <int NL, bool V4, bool PLAIN>
+__global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
+  extern __shared__ float rc_smem[];
+  constexpr int VW = V4 ? 4 : 1;
+  float* v1s = rc_smem;                // [np][E2]
+  float* v2s = v1s + p.r3 * p.E2;      // [np]
+  float* pl = v2s + p.r3;              // [np][E2][E1p]
+  const int g = blockIdx.x / p.nsplit, sp = blockIdx.x - g * p.nsplit;
+  const int i3a = sp * p.r3, np = min(p.r3, p.E3 - i3a);
+  int64_t gb[NL];
+  rc_group_base<NL>(p, g, gb);
+  constexpr int B = PLAIN ? 8 : (NL <= 3 ? 4 : 2);
+  const int units = np * p.E2 * p.U1;
+  for (int u0 = threadIdx.x; u0 < units; u0 += B * blockDim.x) {
+    float4 v[B];
+    int64_t off[B][NL];
+    bool on[B];
+    int dst[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const int u = u0 + k * blockDim.x;
+      on[k] = u < units;
+      uint32_t rest, i1u, pi, i2;
+      p.fU1.divmod((uint32_t)(on[k] ? u : 0), rest, i1u);
+      p.fE2.divmod(rest, pi, i2);
+      const int64_t i3 = i3a + (int)pi, i1 = (int64_t)i1u * VW;
+#pragma unroll
+      for (int l = 0; l < NL; ++l) off[k][l] = gb[l] + i3 * p.s3[l] + (int64_t)i2 * p.s2[l] + i1 * p.s1[l];
+      dst[k] = (int)(pi * p.E2 + i2) * p.E1p + (int)i1;
+    }
+    rc_source<NL, B, V4, PLAIN>(p, off, on, v);
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (on[k]) {
+        pl[dst[k]] = v[k].x;
+        if (V4) {
+          pl[dst[k] + 1] = v[k].y;
+          pl[dst[k] + 2] = v[k].z;
+          pl[dst[k] + 3] = v[k].w;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < np * p.E2; r += blockDim.x) {
+    const float* row = pl + r * p.E1p;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int j = 0;
+    for (; j + 4 <= p.E1; j += 4) {
+      a0 += (double)row[j];
+      a1 += (double)row[j + 1];
+      a2 += (double)row[j + 2];
+      a3 += (double)row[j + 3];
+    }
+    for (; j < p.E1; ++j) a0 += (double)row[j];
+    v1s[r] = rc_epi(p, 0, (float)((a0 + a1) + (a2 + a3)));
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pi = wp; pi < np; pi += nw) {  // stage 2: a warp per plane
+    double a = 0.0;
+    for (int k = lane; k < p.E2; k += 32) a += (double)v1s[pi * p.E2 + k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) {
+      const float v2 = rc_epi(p, 1, (float)a);
+      if (p.nst < 3) p.out[g] = v2;  // E3 == 1
+      else if (p.nsplit == 1) v2s[pi] = v2;
+      else p.ws[(int64_t)g * p.E3 + i3a + pi] = v2;
+    }
+  }
+  if (p.nst < 3) return;
+  if (p.nsplit == 1) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      for (int t = 0; t < p.E3; ++t) a += (double)v2s[t];
+      p.out[g] = rc_epi(p, 2, (float)a);
+    }
+    return;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned ticket = atomicAdd(p.tick + g, 1u);
+    if (ticket == (unsigned)p.nsplit - 1) {  // every block of this group has published
+      __threadfence();
+      const float* w = p.ws + (int64_t)g * p.E3;
+      double a = 0.0;
+      for (int t = 0; t < p.E3; ++t) a += (double)__ldcg(w + t);
+      p.out[g] = rc_epi(p, 2, (float)a);
+      p.tick[g] = 0u;
+    }
+  }
+}
+
+// cols mode (stage 1 over a strided axis, stage 3 over the contiguous one): block (group g, stage-2
+// rows [h0, h0 + nh)) gives a thread each (row, 4 consecutive stage-3 indices) and a slice of the
+// stage-1 axis, walked with 8 loads in flight -- a warp reads contiguous 512-byte spans; slices fold
+// in order through shared memory.  Stage 2 sums the block's rows per column in f64; with several
+// blocks per group those f64 partials meet in the group's last block (ticket), which rounds them,
+// applies the stage-2 epilogue and folds stage 3.
+template <int NL, bool V4, bool PLAIN>
+__global__ void __launch_bounds__(256) redchain_cols(RCArgs p) {
+  extern __shared__ float rc_smem[];
+  constexpr int VW = V4 ? 4 : 1;
+  const int hr = p.r3, W = p.E3;
+  float* v1s = rc_smem;                                                   // [W][hr]
+  float* v2s = v1s + W * hr;                                              // [W]
+  double* part = reinterpret_cast<double*>(rc_smem + ((W * hr + W + 1) & ~1));  // [S][P][VW]
+  const int g = blockIdx.x / p.nsplit, sp = blockIdx.x - g * p.nsplit;
+  const int h0 = sp * hr, nh = min(hr, p.E2 - h0);
+  int64_t gb[NL];
+  rc_group_base<NL>(p, g, gb);
+  const int wu = W / VW;
+  const int npairs = nh * wu;
+  const int pi = threadIdx.x % p.P, si = threadIdx.x / p.P;
+  const int chunk = (p.E1 + p.S - 1) / p.S;
+  const int j0 = si * chunk, j1 = min(p.E1, j0 + chunk);
+  for (int q0 = 0; q0 < npairs; q0 += p.P) {
+    const int q = q0 + pi;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const bool on = q < npairs;
+    const int hl = on ? q / wu : 0, i3 = on ? (q - hl * wu) * VW : 0;
+    if (on) {
+      int64_t po[NL];
+#pragma unroll
+      for (int l = 0; l < NL; ++l) po[l] = gb[l] + (int64_t)i3 * p.s3[l] + (int64_t)(h0 + hl) * p.s2[l];
+      constexpr int B = PLAIN ? 16 : (NL <= 3 ? 4 : 2);
+      for (int j = j0; j < j1; j += B) {
+        float4 v[B];
+        int64_t off[B][NL];
+        bool on[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          on[u] = j + u < j1;
+#pragma unroll
+          for (int l = 0; l < NL; ++l) off[u][l] = po[l] + (int64_t)(j + u) * p.s1[l];
+        }
+        rc_source<NL, B, V4, PLAIN>(p, off, on, v);
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+          if (on[u]) {
+            a0 += (double)v[u].x;
+            if (V4) {
+              a1 += (double)v[u].y;
+              a2 += (double)v[u].z;
+              a3 += (double)v[u].w;
+            }
+          }
+        }
+      }
+    }
+    if (p.S > 1) {
+      double* d = part + ((int64_t)si * p.P + pi) * VW;
+      d[0] = a0;
+      if (V4) {
+        d[1] = a1;
+        d[2] = a2;
+        d[3] = a3;
+      }
+      __syncthreads();
+      if (si == 0 && on) {
+        for (int t = 1; t < p.S; ++t) {
+          const double* e = part + ((int64_t)t * p.P + pi) * VW;
+          a0 += e[0];
+          if (V4) {
+            a1 += e[1];
+            a2 += e[2];
+            a3 += e[3];
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (si == 0 && on) {
+      float* d = v1s + i3 * hr + hl;
+      d[0] = rc_epi(p, 0, (float)a0);
+      if (V4) {
+        d[hr] = rc_epi(p, 0, (float)a1);
+        d[2 * hr] = rc_epi(p, 0, (float)a2);
+        d[3 * hr] = rc_epi(p, 0, (float)a3);
+      }
+    }
+  }
+  __syncthreads();
+  double* wsd = reinterpret_cast<double*>(p.ws);
+  for (int t = threadIdx.x; t < W; t += blockDim.x) {  // stage 2 over this block's rows
+    double a = 0.0;
+    for (int k = 0; k < nh; ++k) a += (double)v1s[t * hr + k];
+    if (p.nsplit == 1) v2s[t] = rc_epi(p, 1, (float)a);
+    else wsd[((int64_t)g * p.nsplit + sp) * W + t] = a;
+  }
+  if (p.nsplit > 1) {
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned last;
+    if (threadIdx.x == 0) last = atomicAdd(p.tick + g, 1u) == (unsigned)p.nsplit - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    for (int t = threadIdx.x; t < W; t += blockDim.x) {
+      double a = 0.0;
+      for (int k = 0; k < p.nsplit; ++k) a += __ldcg(wsd + ((int64_t)g * p.nsplit + k) * W + t);
+      v2s[t] = rc_epi(p, 1, (float)a);
+    }
+    if (threadIdx.x == 0) p.tick[g] = 0u;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    for (int t = 0; t < W; ++t) a += (double)v2s[t];
+    p.out[g] = rc_epi(p, 2, (float)a);
+  }
+}
+
+template <typename K>
+static void rc_smem_attr(K k) {
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
+}
+
+template <int NL, bool PLAIN>
+static void launch_redchain(const RCArgs& p, bool rows, bool v4, int grid, int threads, size_t smem, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    rc_smem_attr(redchain_rows<NL, true, PLAIN>);
+    rc_smem_attr(redchain_rows<NL, false, PLAIN>);
+    rc_smem_attr(redchain_cols<NL, true, PLAIN>);
+    rc_smem_attr(redchain_cols<NL, false, PLAIN>);
+    attr = true;
+  }
+  if (rows) {
+    if (v4) redchain_rows<NL, true, PLAIN><<<grid, threads, smem, s>>>(p);
+    else redchain_rows<NL, false, PLAIN><<<grid, threads, smem, s>>>(p);
+  } else {
+    if (v4) redchain_cols<NL, true, PLAIN><<<grid, threads, smem, s>>>(p);
+    else redchain_cols<NL, false, PLAIN><<<grid, threads, smem, s>>>(p);
+  }
+}
+
 }  // namespace pb
 
 using namespace pb;
@@ -1456,6 +1918,205 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
     case 6: launch_chain<6>(p, mode, s); break;
     case 7: launch_chain<7>(p, mode, s); break;
     default: launch_chain<8>(p, mode, s); break;
+  }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+
+int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                    const pb_chain_step* steps, int src_ndim, const int64_t* src_shape, int nstages,
+                    const pb_red_stage* stages, const pb_tensor* out) {
+  if (nleaves < 1 || nleaves > kChainLeaves || nsteps < 0 || nsteps > kChainSteps || src_ndim < 1 || src_ndim > 4 ||
+      nstages < 1 || nstages > 3)
+    return fail(PB_ERR_ARG, "pb_reduce_chain: bad chain shape");
+  if (out->dtype != PB_F32 || !is_contiguous(*out)) return fail(PB_ERR_ARG, "pb_reduce_chain: out must be dense f32");
+  if (nstages < 2) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: single-stage chains use pb_reduce");
+  RCArgs p;
+  memset(&p, 0, sizeof(p));
+  p.nleaves = nleaves;
+  p.nsteps = nsteps;
+  p.head_kind = head_kind;
+  p.head_scalar = (float)head_scalar;
+  p.out = (float*)(uintptr_t)out->ptr;
+  for (int k = 0; k < nsteps; ++k) {
+    const pb_chain_step& c = steps[k];
+    if (c.kind == 1 && (c.leaf < 0 || c.leaf >= nleaves)) return fail(PB_ERR_ARG, "pb_reduce_chain: bad leaf index");
+    p.step[k].op = (int16_t)c.op;
+    p.step[k].kind = (int8_t)c.kind;
+    p.step[k].side = (int8_t)c.side;
+    p.step[k].leaf = (int8_t)c.leaf;
+    p.step[k].to_bool = (int8_t)c.to_bool;
+    p.step[k].scalar = (float)c.scalar;
+  }
+  // the source index space, left-padded to 4 axes; leaf strides broadcast (right-aligned)
+  const int pad = 4 - src_ndim;
+  int64_t sh[4], st[kChainLeaves][4];
+  for (int k = 0; k < 4; ++k) sh[k] = k < pad ? 1 : src_shape[k - pad];
+  for (int l = 0; l < nleaves; ++l) {
+    const pb_tensor& t = leaves[l];
+    if (t.dtype != PB_F32 && t.dtype != PB_BOOL) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: leaf dtype");
+    const int off = 4 - t.ndim;
+    if (off < 0) return fail(PB_ERR_ARG, "pb_reduce_chain: leaf rank exceeds the source rank");
+    for (int k = 0; k < 4; ++k) st[l][k] = 0;
+    for (int k = 0; k < t.ndim; ++k) {
+      if (t.shape[k] != 1 && t.shape[k] != sh[off + k]) return fail(PB_ERR_ARG, "pb_reduce_chain: leaf shape");
+      st[l][off + k] = t.shape[k] == 1 ? 0 : t.strides[k];
+    }
+    p.leaf[l] = (const void*)(uintptr_t)t.ptr;
+    p.is_bool[l] = t.dtype == PB_BOOL;
+  }
+  int ax[3] = {-1, -1, -1};
+  bool used[4] = {false, false, false, false};
+  for (int k = 0; k < nstages; ++k) {
+    const int a = stages[k].axis + pad;
+    if (a < pad || a > 3 || used[a]) return fail(PB_ERR_ARG, "pb_reduce_chain: bad stage axis");
+    used[a] = true;
+    ax[k] = a;
+    p.epi[k] = stages[k].epi_op;
+    p.epil[k] = stages[k].epi_left;
+    p.epis[k] = stages[k].scalar;
+    if (p.epi[k] >= 0 && p.epi[k] != PB_ADD && p.epi[k] != PB_SUB && p.epi[k] != PB_MUL && p.epi[k] != PB_DIV)
+      return fail(PB_ERR_ARG, "pb_reduce_chain: epilogue must be add/sub/mul/div");
+  }
+  for (int k = nstages; k < 3; ++k) p.epi[k] = -1;
+  p.nst = nstages;
+  // rows: stage 1 over the innermost axis, stage 2 over the next; cols: stage 3 innermost
+  const bool rows = ax[0] == 3 && ax[1] == 2;
+  const bool cols = nstages == 3 && ax[2] == 3;
+  if (!rows && !cols) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: stage axes");
+  p.E1 = (int)sh[ax[0]];
+  p.E2 = (int)sh[ax[1]];
+  p.E3 = nstages == 3 ? (int)sh[ax[2]] : 1;
+  int64_t G = 1;
+  int nk = 0, kax[3] = {-1, -1, -1};
+  for (int k = 0; k < 4; ++k) {
+    if (used[k] || sh[k] == 1) continue;
+    if (nk == 3) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: kept axes");
+    kax[nk++] = k;
+    G *= sh[k];
+  }
+  {  // right-align the kept axes into slots 0..2 (outer first)
+    int64_t kext[3] = {1, 1, 1};
+    for (int j = 0; j < nk; ++j) {
+      const int slot = 3 - nk + j;
+      kext[slot] = sh[kax[j]];
+      for (int l = 0; l < nleaves; ++l) p.ks[l][slot] = st[l][kax[j]];
+    }
+    p.kd1 = FastDiv((uint32_t)kext[1]);
+    p.kd2 = FastDiv((uint32_t)kext[2]);
+  }
+  if (G != numel(*out)) return fail(PB_ERR_ARG, "pb_reduce_chain: output size");
+  if (G == 0) return PB_OK;
+  if (G >= ((int64_t)1 << 31) || sh[0] * sh[1] * sh[2] * sh[3] >= ((int64_t)1 << 40) || p.E2 * (int64_t)p.E3 > 65536)
+    return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: extents");
+  for (int l = 0; l < nleaves; ++l) {
+    p.s1[l] = st[l][ax[0]];
+    p.s2[l] = st[l][ax[1]];
+    p.s3[l] = nstages == 3 ? st[l][ax[2]] : 0;
+  }
+  if (p.E1 == 0 || p.E2 == 0 || p.E3 == 0) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: empty stage");
+  for (int k = 0; k < nsteps; ++k) {  // the reduction's evaluator runs the cheap (non-libm) steps only
+    const int op = steps[k].op;
+    const bool ok = steps[k].kind == 0 ? (op == 64 + PB_NEG || op == 64 + PB_ABS || op == 64 + PB_NOT ||
+                                          op == 64 + PB_CAST)
+                                       : (op != PB_POW && op >= 0 && op <= PB_OR);
+    if (!ok) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: step op outside the reduction evaluator");
+  }
+  // 16-byte vectors along the contiguous axis (stage 1 in rows mode, stage 3 in cols mode)
+  const int vax = rows ? ax[0] : ax[2];
+  bool v4 = sh[vax] % 4 == 0;
+  for (int l = 0; l < nleaves && v4; ++l) {
+    const int64_t vs = st[l][vax];
+    if (vs == 0) continue;
+    if (vs != 1 || leaves[l].ptr % (p.is_bool[l] ? 4 : 16)) v4 = false;
+    for (int k = 0; k < 4; ++k)
+      if (k != vax && st[l][k] % 4) v4 = false;
+  }
+  for (int l = 0; l < nleaves; ++l) p.s_vec[l] = v4 && st[l][vax] == 1;
+  // Which chains this kernel runs is measured (tools/redchain_bench.py): a chain-fed source saves
+  // materialising the chain and always wins; a plain (already materialised) source wins only where
+  // launches dominate -- rows mode with few channels or < 2M elements, cols mode on 16-byte rows
+  // below 4M elements -- elsewhere the stage-at-a-time kernels stream faster: decline
+  static const bool all_sizes = getenv("PB_RC_ALL") != nullptr;  // tools/redchain_bench.py measures both
+  const int64_t numel4 = sh[0] * sh[1] * sh[2] * sh[3];
+  // chains of more than two leaves or with a division stream slower here than as one chain kernel
+  // plus the stage kernels (measured: BatchNorm's grad-of-std chain, 3 leaves and 2 divisions)
+  bool heavy = nleaves > 2;
+  for (int k = 0; k < nsteps; ++k) heavy = heavy || (steps[k].kind != 0 && steps[k].op == PB_DIV);
+  if (!all_sizes && heavy) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: heavy chain");
+  if (!all_sizes && nleaves == 1 && nsteps == 0 && head_kind == 0 &&
+      (rows ? !(G < 256 || numel4 < ((int64_t)1 << 21)) : !(v4 && numel4 < ((int64_t)1 << 22))))
+    return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: plain source streams faster stage by stage");
+  // rows: a block owns one group and `pp` planes (>= ~2K elements); cols: one group and `hr` rows
+  // of stage 2 (~256 threads of work)
+  const int unit = (!rows && v4) ? 4 : 1;
+  int nsplit = 1, r3 = p.E3, threads = 256;
+  size_t smem = 0;
+  if (rows) {
+    p.U1 = v4 ? p.E1 / 4 : p.E1;
+    p.E1p = p.E1 | 1;  // odd pitch: a thread per row reads conflict-free
+    // whole groups in one block (no ticket) when there are enough groups to fill the SMs, else
+    // split the planes so that ~4 blocks per SM run; shared memory caps the planes per block
+    const int64_t plane = (int64_t)p.E2 * p.E1p;
+    const int64_t target = 4 * (int64_t)num_sms();
+    int64_t pp = G * 2 >= target ? p.E3 : (p.E3 + (target + G - 1) / G - 1) / ((target + G - 1) / G);
+    const int64_t cap = (96 * 1024 / 4 - 2 * (int64_t)p.E3 * (p.E2 + 1)) / plane;
+    if (pp > cap) pp = cap > 1 ? cap : 1;
+    if (pp > p.E3) pp = p.E3;
+    if (pp < 1) pp = 1;
+    r3 = (int)pp;
+    nsplit = (p.E3 + r3 - 1) / r3;
+    p.fU1 = FastDiv((uint32_t)p.U1);
+    p.fE2 = FastDiv((uint32_t)p.E2);
+    smem = sizeof(float) * (size_t)(r3 * p.E2 + r3 + r3 * plane);
+    const int64_t units = (int64_t)r3 * p.E2 * p.U1;
+    threads = units >= 1024 ? 256 : units >= 512 ? 128 : 64;
+    if (nsplit > 1 && nstages == 3) {
+      p.ws = (float*)workspace(sizeof(float) * G * p.E3);
+      if (!p.ws) return fail(PB_ERR_OOM, "pb_reduce_chain: workspace");
+    }
+  } else {
+    // one pass of <= 256 (row, column-unit) pairs per block, and >= ~4 blocks per SM: few groups
+    // split their rows further (the threads then split the stage-1 axis into slices)
+    const int wu = p.E3 / unit;
+    int hr = wu >= 256 ? 1 : 256 / wu;  // one pass of <= 256 (row, column-unit) pairs per block
+    if (hr > p.E2) hr = p.E2;
+    r3 = hr;
+    nsplit = (p.E2 + hr - 1) / hr;
+    const int64_t npairs = (int64_t)hr * wu;
+    int P = (int)(npairs >= 256 ? 256 : (npairs + 31) / 32 * 32);
+    int S = 256 / P;
+    if (S > p.E1 / 16) S = p.E1 / 16;
+    if (S < 1) S = 1;
+    p.P = P;
+    p.S = S;
+    threads = P * S;
+    smem = sizeof(float) * (((size_t)p.E3 * hr + p.E3 + 1) & ~(size_t)1);
+    if (S > 1) smem += sizeof(double) * (size_t)P * S * unit;
+    if (nsplit > 1) {
+      p.ws = (float*)workspace(sizeof(double) * G * nsplit * p.E3);
+      if (!p.ws) return fail(PB_ERR_OOM, "pb_reduce_chain: workspace");
+    }
+  }
+  p.r3 = r3;
+  p.nsplit = nsplit;
+  if (nsplit > 1) {
+    p.tick = tick_counters(G);
+    if (!p.tick) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: more groups than ticket counters");
+  }
+  if (smem > 112 * 1024) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: stage tile exceeds shared memory");
+  const int64_t grid = G * nsplit;
+  if (grid >= ((int64_t)1 << 31)) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: grid");
+  cudaStream_t s = compute_stream();
+  const bool plain = nleaves == 1 && nsteps == 0 && head_kind == 0 && !p.is_bool[0];
+  switch (plain ? 0 : nleaves) {
+    case 0: launch_redchain<1, true>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 1: launch_redchain<1, false>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 2: launch_redchain<2, false>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 3: launch_redchain<3, false>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 4: launch_redchain<4, false>(p, rows, v4, (int)grid, threads, smem, s); break;
+    default: launch_redchain<8, false>(p, rows, v4, (int)grid, threads, smem, s); break;
   }
   PB_LAUNCHED();
   return PB_OK;

@@ -48,6 +48,11 @@ void* workspace(size_t bytes) {
   return g_ws;
 }
 
+// zeroed per-group ticket counters for single-launch multi-block reductions; every user
+// resets the counters it took back to zero, so the buffer is all-zero between kernels
+static unsigned* g_ticks = nullptr;
+unsigned* tick_counters(int64_t n) { return n <= kTickCounters ? g_ticks : nullptr; }
+
 // ---- index helpers -----------------------------------------------------------------------
 int64_t numel(const pb_tensor& t) {
   int64_t n = 1;
@@ -150,6 +155,8 @@ int pb_init(int device) {
     g_stage[i].cap = kStageBytes;
     PB_CUDA(cudaEventCreateWithFlags(&g_stage[i].ev, cudaEventDisableTiming));
   }
+  PB_CUDA(cudaMalloc(&g_ticks, sizeof(unsigned) * kTickCounters));
+  PB_CUDA(cudaMemset(g_ticks, 0, sizeof(unsigned) * kTickCounters));
   g_device = device;
   g_inited = true;
   return PB_OK;

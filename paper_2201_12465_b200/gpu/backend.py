@@ -18,6 +18,7 @@ backend cannot be constructed.
 import ctypes
 import os
 import sys
+import struct
 import threading
 import weakref
 
@@ -185,25 +186,58 @@ _INT_RANGE = {"u8": (0, 255), "i32": (-2**31, 2**31 - 1), "i64": (-2**63, 2**63 
 
 
 class LazyReduce:
-    """Adapter of a deferred f32 reduction whose only consumer (per the traced plan) is a
-    scalar add/sub/mul/div: that consumer runs both as one ``pb_reduce_epi`` launch.  Any
-    other use runs the plain reduction first."""
+    """Adapter of a deferred f32 reduction chain (backend-internal fusion).
 
-    __slots__ = ("be", "call", "arg", "shape", "strides", "dtype", "host", "_dev", "__weakref__")
+    ``src`` is the stage-1 input -- a DeviceArray, or a LazyArray whose elementwise chain is
+    evaluated inside the reduction -- and ``stages`` the single-axis reductions applied to it in
+    order, each ``(call, source axis, epilogue)`` with the epilogue an f32 scalar
+    ``(op, scalar, scalar_left)`` or None: the reference's ``mean`` (sum / n, minml/ops.py:33-36)
+    and BatchNorm / _unbroadcast stacks of them (minml/nn.py:288-306, minml/autograd.py:290-297).
+    The traced plan keeps a reduction lazy only while its single consumer extends the chain; the
+    chain then runs as one ``pb_reduce_chain`` (or ``pb_reduce_epi``) launch.  ``cur`` maps the
+    axes of the current result to source axes (keepdims leaves a reduced axis in place)."""
 
-    def __init__(self, be, call, arg):
-        self.be, self.call, self.arg = be, call, arg
-        self.shape = tuple(call.shape)
-        self.strides = contig_strides(self.shape)
-        self.dtype = call.dtype
+    __slots__ = ("be", "src", "stages", "cur", "shape", "strides", "dtype", "host", "_dev", "__weakref__")
+
+    def __init__(self, be, src, stages, cur, shape, dtype):
+        self.be, self.src, self.stages, self.cur = be, src, stages, cur
+        self.shape = shape
+        self.strides = contig_strides(shape)
+        self.dtype = dtype
         self.host = None
         self._dev = None
+
+    @classmethod
+    def first(cls, be, call, src):
+        axis = call.params.get("axis")
+        ax = normalize_axis(axis, len(src.shape))
+        keep = bool(call.params.get("keepdims", False))
+        cur = tuple(range(len(src.shape)))
+        if not keep:
+            cur = cur[:ax] + cur[ax + 1:]
+        return cls(be, src, ((call, ax, None),), cur, tuple(call.shape), call.dtype)
+
+    def extend(self, call):
+        """This chain followed by the f32 sum ``call`` (None when it cannot be expressed)."""
+        if self._dev is not None or call.name != "sum" or call.params.get("axis") is None:
+            return None
+        ax = normalize_axis(call.params["axis"], len(self.shape))
+        sax = self.cur[ax]
+        if len(self.stages) >= 3 or any(st[1] == sax for st in self.stages):
+            return None
+        cur = self.cur if call.params.get("keepdims", False) else self.cur[:ax] + self.cur[ax + 1:]
+        return LazyReduce(self.be, self.src, self.stages + ((call, sax, None),), cur, tuple(call.shape),
+                          call.dtype)
+
+    def with_epi(self, epi):
+        c, ax, _ = self.stages[-1]
+        return LazyReduce(self.be, self.src, self.stages[:-1] + ((c, ax, epi),), self.cur, self.shape, self.dtype)
 
     def dev(self):
         d = self._dev
         if d is None:
-            d = self._dev = self.be._run_reduce(self.call, self.arg)
-            self.arg = None
+            d = self._dev = self.be._run_red_chain(self)
+            self.src = None
         return d
 
     def materialize(self):
@@ -293,6 +327,7 @@ class GpuBackend(Backend):
         self._op_idx = 0
         self._lazy_ok = True
         self._lazy_red = False
+        self._lazy_epi = False
         self._lib = _lib.load()
         _lib.check(self._lib.pb_init(device), "pb_init")
         self.device = device
@@ -393,7 +428,9 @@ class GpuBackend(Backend):
 
     def _execute(self, call, args):
         name = call.name
-        if name not in _FUSE_BIN and name not in _FUSE_UN:
+        if name == "sum":
+            pass  # _reduce extends or runs lazy sources itself
+        elif name not in _FUSE_BIN and name not in _FUSE_UN:
             args = [a.dev() if type(a) is LazyArray or type(a) is LazyReduce else a for a in args]
         elif type(args[0]) is LazyReduce and not (name in _EPI and "scalar" in call.params):
             args = [a.dev() if type(a) is LazyReduce else a for a in args]
@@ -422,12 +459,14 @@ class GpuBackend(Backend):
         prods = tuple(self._producer(a) for a in args)
         if self._trace is not None:
             epi = name in _EPI and "scalar" in call.params and call.dtype is dtypes.f32
-            self._trace.append((sig, prods, fusible, epi))
+            red_ax = name == "sum" and call.dtype is dtypes.f32 and call.params.get("axis") is not None
+            self._trace.append((sig, prods, fusible, epi, red_ax))
         else:
-            tr, lazy, lazy_red = self._plan
+            tr, lazy, lazy_red, lazy_epi = self._plan
             if idx < len(tr) and tr[idx][0] == sig and tr[idx][1] == prods:
                 self._lazy_ok = lazy[idx]
                 self._lazy_red = lazy_red[idx]
+                self._lazy_epi = lazy_epi[idx]
             else:  # the step diverged from the trace: stop fusing (everything materialises)
                 self._abandon_plan()
         res = self._execute(call, args)
@@ -449,23 +488,41 @@ class GpuBackend(Backend):
         self._trace, self._prod, self._op_idx = [], {}, 0
 
     def fusion_trace_end(self):
-        """Build the plan: an elementwise f32/bool result may stay lazy iff the traced step
-        consumed it exactly once, by an elementwise op.  Returns the number of such ops."""
+        """Build the plan from the traced step's single-consumer links:
+
+        * an elementwise f32/bool result stays lazy iff it was consumed exactly once, by an
+          elementwise op, or by an f32 sum that opens a multi-stage reduction chain (the chain is
+          then evaluated inside the reduction);
+        * an f32 sum/max/min stays lazy iff its one consumer is a scalar add/sub/mul/div (mean =
+          sum / n) or -- for a sum -- another f32 sum over an axis;
+        * such a scalar op on a lazy sum stays lazy iff its one consumer is an f32 sum.
+        Returns the number of lazy results."""
         tr, self._trace, self._prod = self._trace, None, {}
         n = len(tr)
-        uses, by_fusible, by_epi = [0] * n, [True] * n, [True] * n
-        for sig, prods, fusible, epi in tr:
+        uses, by_fusible, cons = [0] * n, [True] * n, [-1] * n
+        for j, (sig, prods, fusible, epi, red_ax) in enumerate(tr):
             for q in prods:
                 if q >= 0:
                     uses[q] += 1
                     by_fusible[q] = by_fusible[q] and fusible
-                    by_epi[q] = by_epi[q] and epi
-        lazy = [tr[i][2] and uses[i] == 1 and by_fusible[i] for i in range(n)]
-        # f32 sum/max/min whose one consumer is a scalar add/sub/mul/div (mean = sum / n)
-        lazy_red = [tr[i][0][0] in ("sum", "max_reduce", "min_reduce") and tr[i][0][2] == "f32" and
-                    uses[i] == 1 and by_epi[i] for i in range(n)]
-        self._plan = (tr, lazy, lazy_red)
-        return sum(lazy) + sum(lazy_red)
+                    cons[q] = j
+        one = [uses[i] == 1 for i in range(n)]
+        is_epi = [t[3] for t in tr]
+        is_sum = [t[4] for t in tr]
+        lazy_red = [tr[i][0][0] in ("sum", "max_reduce", "min_reduce") and tr[i][0][2] == "f32" and one[i] and
+                    (is_epi[cons[i]] or (is_sum[i] and is_sum[cons[i]])) for i in range(n)]
+        lazy_epi = [is_epi[i] and one[i] and is_sum[cons[i]] and tr[i][1][0] >= 0 and lazy_red[tr[i][1][0]] and
+                    is_sum[tr[i][1][0]] for i in range(n)]
+
+        def opens_chain(c):  # sum c is the first stage of a chain of >= 2 reductions
+            if not (is_sum[c] and lazy_red[c]):
+                return False
+            d = cons[c]
+            return is_sum[d] or (lazy_epi[d] and is_sum[cons[d]])
+
+        lazy = [tr[i][2] and one[i] and (by_fusible[i] or opens_chain(cons[i])) for i in range(n)]
+        self._plan = (tr, lazy, lazy_red, lazy_epi)
+        return sum(lazy) + sum(lazy_red) + sum(lazy_epi)
 
     def fusion_plan_begin(self):
         """Replay the planned step (normally while recording a CUDA graph): ops the plan marks
@@ -479,7 +536,8 @@ class GpuBackend(Backend):
     def _abandon_plan(self):
         self._lazy_ok = False
         self._lazy_red = False
-        self._plan = ([], [], [])
+        self._lazy_epi = False
+        self._plan = ([], [], [], [])
 
     @property
     def plan_abandoned(self):
@@ -492,6 +550,7 @@ class GpuBackend(Backend):
             self._fuse = self._fuse_saved
         self._lazy_ok = True
         self._lazy_red = False
+        self._lazy_epi = False
 
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
@@ -822,10 +881,12 @@ class GpuBackend(Backend):
         if type(args[0]) is LazyReduce:
             lr = args[0]
             s = p["scalar"]
-            if (lr._dev is None and type(s) in (int, float) and call.dtype is dtypes.f32 and
-                    compute_dtype(name, lr.dtype, s, True) is dtypes.f32 and abs(float(s)) <= 3.4e38):
+            if (lr._dev is None and lr.stages[-1][2] is None and type(s) in (int, float) and
+                    call.dtype is dtypes.f32 and compute_dtype(name, lr.dtype, s, True) is dtypes.f32 and
+                    abs(float(s)) <= 3.4e38):
                 # (a later use of the plain reduction -- none per the plan -- would recompute it)
-                return self._run_reduce(lr.call, lr.arg, (name, float(s), p.get("scalar_side") == "left"))
+                nl = lr.with_epi((name, float(s), p.get("scalar_side") == "left"))
+                return nl if self._lazy_epi else nl.dev()
             args = [lr.dev()]
         if name == "mul" and "scalar" not in p:
             view = self._times_one(call, args)
@@ -922,9 +983,51 @@ class GpuBackend(Backend):
 
     # reductions
     def _reduce(self, call, args):
-        if self._lazy_red and call.shape.size > 0 and args[0].dtype is dtypes.f32:
-            return LazyReduce(self, call, args[0])
-        return self._run_reduce(call, args[0])
+        a = args[0]
+        if type(a) is LazyReduce:
+            nl = a.extend(call) if call.shape.size > 0 else None
+            if nl is None:
+                return self._run_reduce(call, a.dev())
+            return nl if self._lazy_red else nl.dev()
+        if type(a) is LazyArray:
+            if self._lazy_red and call.name == "sum" and call.shape.size > 0 and a.dtype is dtypes.f32 and \
+                    call.params.get("axis") is not None:
+                return LazyReduce.first(self, call, a)
+            a = a.dev()
+        if self._lazy_red and call.shape.size > 0 and a.dtype is dtypes.f32:
+            return LazyReduce.first(self, call, a) if call.params.get("axis") is not None else \
+                LazyReduce(self, a, ((call, -1, None),), (), tuple(call.shape), call.dtype)
+        return self._run_reduce(call, a)
+
+    def _run_red_chain(self, lr):
+        """Run a LazyReduce: one pb_reduce_chain launch for 2-3 stages, else (or when the kernel
+        declines the layout) the stages one by one exactly as the eager path runs them."""
+        src = lr.src
+        if len(lr.stages) >= 2 and len(src.shape) <= 4:
+            out = self._new(lr.shape, dtypes.f32, "sum")
+            if out.block is None:
+                return out
+            if type(src) is LazyArray and src._dev is None:
+                leaves, head, steps = src.leaves, src.head, src.steps
+            else:
+                leaves, head, steps = (src.dev() if type(src) is LazyArray else src,), ("leaf", 0), ()
+            lv = b"".join(d.packed() for d in leaves)
+            sp = b"".join(_lib.STEP.pack(op, kind, side, leaf, tb, 0, sc) for op, kind, side, leaf, tb, sc in steps)
+            hk, hv = (0, 0.0) if head[0] == "leaf" else (1, float(head[1]))
+            stg = b"".join(_lib.RSTAGE.pack(ax, -1, 0, 0.0) if epi is None else
+                           _lib.RSTAGE.pack(ax, _lib.BINOP[epi[0]], 1 if epi[2] else 0, epi[1])
+                           for _, ax, epi in lr.stages)
+            shp = struct.pack(f"<{len(src.shape)}q", *src.shape)
+            rc = self._lib.pb_reduce_chain(len(leaves), lv, hk, hv, len(steps), sp, len(src.shape), shp,
+                                           len(lr.stages), stg, out.packed())
+            if rc == 0:
+                return out
+            if rc != _lib.UNSUPPORTED:
+                _lib.check(rc, "reduce chain")
+        x = src.dev() if type(src) is LazyArray else src
+        for call, _, epi in lr.stages:
+            x = self._run_reduce(call, x, epi)
+        return x
 
     def _run_reduce(self, call, a, epi=None):
         """The reduction; with ``epi = (op, scalar, scalar_left)`` its f32 scalar consumer too."""
