@@ -24,7 +24,8 @@ extern "C" {
 #endif
 
 enum pb_status { PB_OK = 0, PB_ERR_CUDA = 1, PB_ERR_ARG = 2, PB_ERR_OOM = 3, PB_ERR_ALLOC = 4,
-                 PB_ERR_DOMAIN = 5, PB_ERR_NCCL = 6, PB_ERR_UNSUPPORTED = 7 };
+                 PB_ERR_DOMAIN = 5, PB_ERR_NCCL = 6, PB_ERR_UNSUPPORTED = 7,
+                 PB_ERR_TIMEOUT = 8 };
 
 /* element types; codes equal the reference's promotion rank (minml/dtypes.py:41-46) */
 enum pb_dtype { PB_BOOL = 0, PB_U8 = 1, PB_I32 = 2, PB_I64 = 3, PB_F32 = 4, PB_F64 = 5 };
@@ -190,6 +191,17 @@ int pb_nccl_allreduce(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t c
 int pb_nccl_broadcast(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t count, int dtype, int root);
 int pb_nccl_allgather(void* comm, uint64_t sendbuf, uint64_t recvbuf, uint64_t count, int dtype);
 int pb_nccl_wait(void* comm);  /* compute stream waits for everything enqueued on the comm stream */
+/* Collective watchdog (the reference's CollectiveTimeout, minml/distributed.py:23,93-105): the
+ * host waits at most timeout_ms for the comm stream's queued work; on an NCCL async error or the
+ * deadline the communicator is aborted (ncclCommAbort -- a hung peer would otherwise block the
+ * process forever) and PB_ERR_NCCL / PB_ERR_TIMEOUT is returned.  comm may be NULL (no abort). */
+int pb_nccl_sync(void* comm, int64_t timeout_ms);
+/* test hook: occupy the comm stream for ms milliseconds (a stand-in for a peer that never arrives) */
+int pb_debug_stall_comm(int64_t ms);
+
+/* ---- NVTX ranges: step phases on an Nsight timeline (no-ops unless a tool is attached) ---- */
+int pb_nvtx_push(const char* name);
+int pb_nvtx_pop(void);
 
 /* ---- introspection ------------------------------------------------------------------ */
 uint64_t pb_launch_count(void);  /* kernels launched by this library so far */

@@ -2,7 +2,9 @@
 // minml/distributed.py:129-175).  Collectives run on the comm stream after an event fence
 // on the compute stream; pb_nccl_wait makes the compute stream wait for them.
 #include <nccl.h>
+#include <chrono>
 #include <cstring>
+#include <thread>
 #include "common.cuh"
 
 using namespace pb;
@@ -35,6 +37,16 @@ static int fence(cudaEvent_t* ev, cudaStream_t from, cudaStream_t to) {
 }
 
 static int fence_compute_to_comm() { return fence(&g_to_comm, compute_stream(), comm_stream()); }
+
+// spins on the global nanosecond timer (pb_debug_stall_comm)
+__global__ void stall_kernel(uint64_t ns) {
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  do {
+    __nanosleep(1000);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  } while (t - t0 < ns);
+}
 
 extern "C" {
 
@@ -90,6 +102,39 @@ int pb_nccl_allgather(void* comm, uint64_t send, uint64_t recv, uint64_t count, 
 int pb_nccl_wait(void* comm) {
   (void)comm;
   return fence(&g_to_compute, comm_stream(), compute_stream());
+}
+
+int pb_nccl_sync(void* comm, int64_t timeout_ms) {
+  static cudaEvent_t done = nullptr;
+  if (!done) PB_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  PB_CUDA(cudaEventRecord(done, comm_stream()));
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms);
+  for (;;) {
+    const cudaError_t q = cudaEventQuery(done);
+    if (q == cudaSuccess) return PB_OK;
+    if (q != cudaErrorNotReady) return cuda_fail(q, "pb_nccl_sync");
+    if (comm) {
+      ncclResult_t ar = ncclSuccess;
+      ncclCommGetAsyncError((ncclComm_t)comm, &ar);
+      if (ar != ncclSuccess && ar != ncclInProgress) {
+        ncclCommAbort((ncclComm_t)comm);
+        return fail(PB_ERR_NCCL, std::string("collective failed: ") + ncclGetErrorString(ar) +
+                                     " (communicator aborted)");
+      }
+    }
+    if (std::chrono::steady_clock::now() >= deadline) {
+      if (comm) ncclCommAbort((ncclComm_t)comm);
+      return fail(PB_ERR_TIMEOUT, "collective did not complete within " + std::to_string(timeout_ms) +
+                                      " ms" + (comm ? " (communicator aborted)" : ""));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+int pb_debug_stall_comm(int64_t ms) {
+  stall_kernel<<<1, 1, 0, comm_stream()>>>((uint64_t)ms * 1000000ull);
+  PB_LAUNCHED();
+  return PB_OK;
 }
 
 }  // extern "C"

@@ -6,6 +6,7 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <nvtx3/nvToolsExt.h>
 #include "common.cuh"
 
 namespace pb {
@@ -320,3 +321,13 @@ int pb_timer(int op, uint64_t* handle, float* ms) {
 }
 
 }  // extern "C"
+
+// ---- NVTX ranges (named phases of a step on the timeline; no-ops without a tool attached) ----
+extern "C" int pb_nvtx_push(const char* name) {
+  nvtxRangePushA(name ? name : "");
+  return PB_OK;
+}
+extern "C" int pb_nvtx_pop(void) {
+  nvtxRangePop();
+  return PB_OK;
+}

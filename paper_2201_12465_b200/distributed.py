@@ -96,7 +96,7 @@ class Communicator:
         if self.world_size == 1:
             return tensor
         if self._device(tensor):
-            return self._backend(tensor).nccl_all_reduce(self._nccl, tensor, op)
+            return self._backend(tensor).nccl_all_reduce(self._nccl, tensor, op, timeout=self._timeout)
         import torch
         import torch.distributed as dist
         host = np.ascontiguousarray(tensor.to_host_buffer())
@@ -109,7 +109,7 @@ class Communicator:
         if self.world_size == 1:
             return tensor.reshape((1,) + tuple(tensor.shape))
         if self._device(tensor):
-            return self._backend(tensor).nccl_all_gather(self._nccl, tensor, self.world_size)
+            return self._backend(tensor).nccl_all_gather(self._nccl, tensor, self.world_size, timeout=self._timeout)
         import torch
         import torch.distributed as dist
         host = torch.from_numpy(np.ascontiguousarray(tensor.to_host_buffer()).copy())
@@ -141,7 +141,7 @@ class Communicator:
             if tensor is None or tuple(tensor.shape) != shape or tensor.dtype.name != dtname:
                 tensor = T.zeros(shape, dtype=dtname, backend=backend)
         if self._device(tensor):
-            return self._backend(tensor).nccl_broadcast(self._nccl, tensor, root)
+            return self._backend(tensor).nccl_broadcast(self._nccl, tensor, root, timeout=self._timeout)
         import torch
         import torch.distributed as dist
         buf = torch.from_numpy(np.ascontiguousarray(tensor.to_host_buffer()).copy())
@@ -280,6 +280,8 @@ class DataParallel:
         reduced, averaged = flight
         be = registry.get(reduced.backend_id)
         if hasattr(be, "nccl_wait") and self.comm._nccl is not None:
+            if b == 0:  # every bucket is queued by now: one watchdog wait covers them all
+                be.nccl_sync(self.comm._nccl, self.comm._timeout)
             be.nccl_wait(self.comm._nccl)
         avg = reduced if averaged else reduced / self.comm.world_size
         off = 0

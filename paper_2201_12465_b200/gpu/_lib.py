@@ -10,7 +10,7 @@ import ctypes
 import os
 import struct
 
-from ..errors import AllocError, DeviceError, DomainError, OutOfMemory
+from ..errors import AllocError, CollectiveTimeout, DeviceError, DomainError, OutOfMemory
 
 _HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB_PATH = os.environ.get("PB_LIB", os.path.join(_HERE, "libpaper_b200.so"))
@@ -112,6 +112,10 @@ SIGNATURES = {
     "pb_nccl_broadcast": (_I, [_P, _U64, _U64, _U64, _I, _I]),
     "pb_nccl_allgather": (_I, [_P, _U64, _U64, _U64, _I]),
     "pb_nccl_wait": (_I, [_P]),
+    "pb_nccl_sync": (_I, [_P, ctypes.c_int64]),
+    "pb_nvtx_push": (_I, [_B]),
+    "pb_nvtx_pop": (_I, []),
+    "pb_debug_stall_comm": (_I, [ctypes.c_int64]),
     "pb_launch_count": (_U64, []),
     "pb_gemm_path": (_I, []),
     "pb_set_gemm_path": (_I, [_I]),
@@ -149,7 +153,7 @@ def load():
     return _lib
 
 
-_STATUS_EXC = {3: OutOfMemory, 4: AllocError, 5: DomainError}
+_STATUS_EXC = {3: OutOfMemory, 4: AllocError, 5: DomainError, 8: CollectiveTimeout}
 UNSUPPORTED = 7  # PB_ERR_UNSUPPORTED: the entry point declined the layout, nothing was launched
 
 

@@ -25,7 +25,7 @@ import weakref
 import numpy as np
 
 from .. import dtypes
-from ..errors import DeviceError, DomainError, DTypeError, OutOfMemory
+from ..errors import CollectiveTimeout, DeviceError, DomainError, DTypeError, OutOfMemory
 from ..memory import CachingManager, MemoryManager, op_tag
 from ..registry import Backend
 from ..shape import normalize_axis
@@ -1167,18 +1167,39 @@ class GpuBackend(Backend):
 
     _NCCL_OPS = {"sum": 0, "max": 1, "avg": 2}
 
-    def nccl_all_reduce(self, comm, tensor, op="sum", wait=True):
+    _aborted = set()  # communicators the watchdog aborted (any later use raises CollectiveTimeout)
+
+    def _live(self, comm):
+        if comm in GpuBackend._aborted:
+            raise CollectiveTimeout("the NCCL communicator was aborted by the collective watchdog")
+
+    def nccl_sync(self, comm, timeout):
+        """Collective watchdog (minml/distributed.py:23, 93-105 CollectiveTimeout): block until
+        the comm stream's queued collectives finish, at most ``timeout`` seconds; a hung or
+        failed collective aborts the communicator (pb_nccl_sync) and raises CollectiveTimeout /
+        DeviceError instead of hanging the process.  A no-op while a graph is being recorded."""
+        if self._capture_pool or timeout is None:
+            return
+        rc = self._lib.pb_nccl_sync(comm, int(max(0.0, float(timeout)) * 1000))
+        if rc:
+            if comm:
+                GpuBackend._aborted.add(comm)
+            _lib.check(rc, "collective watchdog")
+
+    def nccl_all_reduce(self, comm, tensor, op="sum", wait=True, timeout=None):
         """ncclAllReduce on the comm stream (after a compute->comm fence).  ``op`` "avg" is
         ncclAvg: for the power-of-two worlds of one node the 1/N scale is exact, so it equals
         the reference's sum-then-divide (minml/distributed.py:216-222) bit for bit.  With
         ``wait=False`` the compute stream is not joined: call ``nccl_wait`` before reading
         the result; the source stays referenced until then, and both blocks are recorded
         on the comm stream so an early free parks them behind a comm-stream event."""
+        self._live(comm)
         a = self._contig(tensor.adapter)
         out = self._new(a.shape, a.dtype, "all_reduce")
         _lib.check(self._lib.pb_nccl_allreduce(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code,
                                                self._NCCL_OPS[op]), "ncclAllReduce")
         if wait:
+            self.nccl_sync(comm, timeout)
             self.nccl_wait(comm)
         else:
             out.host = None
@@ -1193,19 +1214,23 @@ class GpuBackend(Backend):
         _lib.check(self._lib.pb_nccl_wait(comm), "nccl wait")
         self._inflight = []
 
-    def nccl_all_gather(self, comm, tensor, world):
+    def nccl_all_gather(self, comm, tensor, world, timeout=None):
+        self._live(comm)
         a = self._contig(tensor.adapter)
         out = self._new((world,) + a.shape, a.dtype, "all_gather")
         _lib.check(self._lib.pb_nccl_allgather(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code),
                    "ncclAllGather")
+        self.nccl_sync(comm, timeout)
         self.nccl_wait(comm)
         return self._tensor(out, (world,) + tuple(tensor.shape))
 
-    def nccl_broadcast(self, comm, tensor, root):
+    def nccl_broadcast(self, comm, tensor, root, timeout=None):
+        self._live(comm)
         a = self._contig(tensor.adapter)
         out = self._new(a.shape, a.dtype, "broadcast")
         _lib.check(self._lib.pb_nccl_broadcast(comm, a.ptr, out.ptr, tensor.shape.size, a.dtype.code, root),
                    "ncclBroadcast")
+        self.nccl_sync(comm, timeout)
         self.nccl_wait(comm)
         return self._tensor(out, tuple(tensor.shape))
 

@@ -18,6 +18,28 @@ def model_backend(model):
     return params[0].backend_id
 
 
+class _Phase:
+    """NVTX range around a step phase on the GPU backend (pb_nvtx_push/pop; a no-op elsewhere
+    and unless an Nsight tool is attached)."""
+
+    __slots__ = ("lib", "name")
+
+    def __init__(self, backend_id, name):
+        be = registry.get(backend_id) if backend_id in registry.registered_ids() else None
+        self.lib = getattr(be, "_lib", None) if hasattr(be, "nccl_sync") else None
+        self.name = name.encode()
+
+    def __enter__(self):
+        if self.lib is not None:
+            self.lib.pb_nvtx_push(self.name)
+        return self
+
+    def __exit__(self, *exc):
+        if self.lib is not None:
+            self.lib.pb_nvtx_pop()
+        return False
+
+
 def train_step(model, images, labels, optimizer, comm=None, on_loss=None, ddp=None):
     """H2D, zero_grad, forward, cross-entropy, backward, [grad sync], step, loss D2H.
 
@@ -26,21 +48,25 @@ def train_step(model, images, labels, optimizer, comm=None, on_loss=None, ddp=No
     allreduces with the backward pass.
     """
     backend = model_backend(model)
-    x = Variable(T.tensor(images, backend=backend))
-    y = T.tensor(labels, backend=backend)
+    with _Phase(backend, "h2d"):
+        x = Variable(T.tensor(images, backend=backend))
+        y = T.tensor(labels, backend=backend)
     optimizer.zero_grad()
-    out = model(x)
-    loss = nn.cross_entropy(out, y)
+    with _Phase(backend, "forward"):
+        out = model(x)
+        loss = nn.cross_entropy(out, y)
     if on_loss is not None:
         on_loss(loss)
-    if ddp is not None:
-        ddp.backward(loss)
-    else:
-        loss.backward()
-        if comm is not None:
-            from .distributed import data_parallel_sync
-            data_parallel_sync(comm, optimizer.params)
-    optimizer.step()
+    with _Phase(backend, "backward+allreduce" if (ddp is not None or comm is not None) else "backward"):
+        if ddp is not None:
+            ddp.backward(loss)
+        else:
+            loss.backward()
+            if comm is not None:
+                from .distributed import data_parallel_sync
+                data_parallel_sync(comm, optimizer.params)
+    with _Phase(backend, "optimizer"):
+        optimizer.step()
     return loss.scalar(), out
 
 

@@ -130,3 +130,32 @@ def test_captured_step_rerecords_on_lr_change():
     assert runs[0][0] == runs[1][0]
     for a, b in zip(runs[0][1], runs[1][1]):
         assert np.array_equal(a, b)
+
+
+def test_collective_watchdog_times_out_and_aborts():
+    """A collective that never completes (the comm stream held by a stall kernel, standing in
+    for a peer that never arrives) raises CollectiveTimeout after the communicator's timeout
+    -- the reference's failure semantics (minml/distributed.py:23, 93-105) -- instead of hanging;
+    the aborted communicator refuses further collectives."""
+    import time
+
+    from paper_2201_12465_b200.errors import CollectiveTimeout
+    from paper_2201_12465_b200.gpu import _lib
+    be = gpu_backend()
+    lib = _lib.load()
+    # the bare watchdog: a 1.5 s stall against a 100 ms deadline, then against a generous one
+    assert lib.pb_debug_stall_comm(1500) == 0
+    t0 = time.perf_counter()
+    assert lib.pb_nccl_sync(None, 100) == 8  # PB_ERR_TIMEOUT
+    assert time.perf_counter() - t0 < 1.0
+    assert lib.pb_nccl_sync(None, 10000) == 0
+    # through the Communicator / backend on a fresh world-1 NCCL communicator
+    comm = distributed.nccl_communicator(0, 1, distributed.nccl_unique_id(), timeout=0.2)
+    x = T.tensor(np.arange(8, dtype=np.float32), backend=be.name)
+    assert np.array_equal(be.nccl_all_reduce(comm._nccl, x, "sum", timeout=comm._timeout).numpy(), x.numpy())
+    assert lib.pb_debug_stall_comm(1500) == 0
+    with pytest.raises(CollectiveTimeout):
+        be.nccl_all_reduce(comm._nccl, x, "sum", timeout=comm._timeout)
+    with pytest.raises(CollectiveTimeout):
+        be.nccl_broadcast(comm._nccl, x, 0, timeout=comm._timeout)
+    be.synchronize()
