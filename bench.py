@@ -209,7 +209,7 @@ def resnet50_convs(n):
 
 
 def kernel_roofline(be, T, hbm_peak, tc_peak):
-    """Live CUDA-event timing of the step's dominant kernel class -- the conv2d family
+    """Live CUDA-event timing (graph replay: device time, no host dispatch) of the step's dominant kernel class -- the conv2d family
     (fprop + dgrad + wgrad of all 53 ResNet-50 convs, less the stem's dgrad that autograd
     skips, hi/lo pre-passes included: 770 GFLOP per step) -- plus the HBM-bound broadcast subtract beside it."""
     rng = np.random.default_rng(5)
@@ -228,12 +228,19 @@ def kernel_roofline(be, T, hbm_peak, tc_peak):
             del ops["dgrad"]
         for name, fn in ops.items():
             fn()
+            # device time of the op as the step runs it: recorded into a CUDA graph, replayed
+            be.synchronize()
             l0 = be.launch_count()
-            stop = be.event_timer()
-            for _ in range(3):
-                fn()
-            ms = stop() / 3
+            be.capture_begin()
+            keep = [fn() for _ in range(3)]
+            graph = be.capture_end()
             launches += cnt * (be.launch_count() - l0) // 3
+            graph.launch()
+            be.synchronize()
+            stop = be.event_timer()
+            graph.launch()
+            ms = stop() / 3
+            del keep, graph
             per[name] += cnt * ms
             total_ms += cnt * ms
             total_flops += cnt * flops

@@ -184,6 +184,8 @@ struct Prob {
   int ti, tj, ntiles, zdim;
   FastDiv fP, fWO;     // output pixel decode (ho*wo, wo)
   int plain;           // 1x1, stride 1, no padding: A is a plain [pixels][C] plane (tiled TMA)
+  int noload;          // diagnostics (PB_TMA_NOLOAD=1): stages are released without loading -- the
+                       // MMA/drain pipeline alone, timed by tools/conv_table.py (results are garbage)
 };
 
 template <int BN, bool WG>
@@ -193,9 +195,14 @@ struct Cfg {
   static constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
   static constexpr int STAGES = (200 * 1024) / STAGE;
   static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
-  static constexpr int NDRAIN = BN / 16;
+  // drain warps: one per (TMEM lane quadrant, 32 accumulator columns) -- each thread folds 32
+  // columns of a chunk, so a chunk drains in about the time the MMA needs for the next one
+  static constexpr int NDRAIN = BN / 8;
   static constexpr int THREADS = 64 + NDRAIN * 32;
-  static constexpr int TMEM_COLS = 4 * BN;
+  // TMEM chunk buffers ({big, small} x BN columns each) in the 512 columns: the MMA may run up to
+  // NBUF - 1 chunks ahead of the drain
+  static constexpr int NBUF = 512 / (2 * BN) < 4 ? 512 / (2 * BN) : 4;
+  static constexpr int TMEM_COLS = NBUF * 2 * BN;
   static constexpr uint32_t IDESC = idesc(BM, BN, false);
 };
 
@@ -255,8 +262,8 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
   uint64_t* accf = empty + C::STAGES;
-  uint64_t* acce = accf + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  uint64_t* acce = accf + C::NBUF;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + C::NBUF);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int per_z = pr.ti * pr.tj;
@@ -267,7 +274,7 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < C::NBUF; ++s) {
       mbar_init(&accf[s], 1);
       mbar_init(&acce[s], C::NDRAIN * 32);
     }
@@ -323,6 +330,10 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
           const int s = it % C::STAGES;
           if (it >= (uint32_t)C::STAGES) mbar_wait(&empty[s], ((it / C::STAGES) - 1) & 1);
           const uint32_t base = smem_u32(smem + s * C::STAGE);
+          if (pr.noload) {
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_expect_tx(&full[s], C::STAGE);
           const int k0 = kbeg + kb * BK;
           if (!WG) {
@@ -354,53 +365,56 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===== MMA issuer (one thread) =====
-    if ((tid & 31) == 0) {
-      uint32_t it = 0, cc = 0;
-      for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
-        int kbeg, kend;
-        krange(t, kbeg, kend);
-        const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-        uint32_t dbig = 0, dsmall = 0;
-        for (int kb = 0; kb < nkb; ++kb, ++it) {
-          const int s = it % C::STAGES;
-          const bool first = (kb % CK) == 0;
-          if (first) {
-            const uint32_t buf = cc & 1;
-            if (cc >= 2) {
-              mbar_wait(&acce[buf], ((cc >> 1) - 1) & 1);
-              tc_fence_after();
-            }
-            dbig = tmem + buf * 2 * BN;
-            dsmall = dbig + BN;
+    // ===== MMA issuer: the whole warp walks the pipeline (warp-uniform values stay in uniform
+    // registers), one elected lane issues.  Stage descriptors are precomputed: within the 128B
+    // swizzle atom a k step of 8 tf32 (32 bytes) is +2 in the descriptor's address field. =====
+    const uint64_t d0 = desc_kmajor(smem_u32(smem));
+    const uint64_t dstage = (uint64_t)(C::STAGE >> 4);
+    const uint64_t dalo = (uint64_t)(C::A_BYTES >> 4), dbhi = (uint64_t)((2 * C::A_BYTES) >> 4);
+    const uint64_t dblo = (uint64_t)((2 * C::A_BYTES + C::B_BYTES) >> 4);
+    uint32_t it = 0, cc = 0;
+    for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
+      int kbeg, kend;
+      krange(t, kbeg, kend);
+      const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+      uint32_t dbig = 0, dsmall = 0;
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % C::STAGES;
+        const bool first = (kb % CK) == 0;
+        if (first) {
+          const uint32_t buf = cc % C::NBUF;
+          if (cc >= (uint32_t)C::NBUF && pr.noload < 4) {
+            mbar_wait(&acce[buf], ((cc / C::NBUF) - 1) & 1);
+            tc_fence_after();
           }
-          mbar_wait(&full[s], (it / C::STAGES) & 1);
-          tc_fence_after();
-          const uint32_t base = smem_u32(smem + s * C::STAGE);
+          dbig = tmem + buf * 2 * BN;
+          dsmall = dbig + BN;
+        }
+        mbar_wait(&full[s], (it / C::STAGES) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint64_t ds = d0 + (uint64_t)s * dstage;
+          if (pr.noload < 3) {  // (diagnostics: PB_TMA_NOLOAD=3 skips the MMAs)
 #pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk) {
-            const uint32_t adv = kk * 32;  // 8 tf32 along the 128-byte swizzled row
-            const uint64_t ahi = desc_kmajor(base + adv), alo = desc_kmajor(base + C::A_BYTES + adv);
-            const uint64_t bhi = desc_kmajor(base + 2 * C::A_BYTES + adv);
-            const uint64_t blo = desc_kmajor(base + 2 * C::A_BYTES + C::B_BYTES + adv);
-            const uint32_t acc = !(first && kk == 0);
-            mma_tf32(dsmall, alo, bhi, C::IDESC, acc);
-            mma_tf32(dsmall, ahi, blo, C::IDESC, 1);
-            mma_tf32(dbig, ahi, bhi, C::IDESC, acc);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t ahi = ds + 2 * kk, alo = ahi + dalo, bhi = ahi + dbhi, blo = ahi + dblo;
+              const uint32_t acc = !(first && kk == 0);
+              mma_tf32(dsmall, alo, bhi, C::IDESC, acc);
+              mma_tf32(dsmall, ahi, blo, C::IDESC, 1);
+              mma_tf32(dbig, ahi, bhi, C::IDESC, acc);
+            }
           }
           mma_commit(&empty[s]);
-          if ((kb % CK) == CK - 1 || kb == nkb - 1) {
-            mma_commit(&accf[cc & 1]);
-            ++cc;
-          }
+          if (((kb % CK) == CK - 1 || kb == nkb - 1) && pr.noload < 4) mma_commit(&accf[cc % C::NBUF]);
         }
+        __syncwarp();
+        if ((kb % CK) == CK - 1 || kb == nkb - 1) ++cc;
       }
     }
-    __syncwarp();
   } else {
-    // ===== drain + epilogue: TMEM lane quadrant is fixed by warp % 4 =====
+    // ===== drain + epilogue: TMEM lane quadrant is fixed by warp % 4, 32 columns per warp =====
     const int q = warp & 3, cg = (warp - 2) >> 2;
-    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cg * 64);
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cg * 32);
     uint32_t cc = 0;
     for (int t = blockIdx.x; t < pr.ntiles; t += gridDim.x) {
       const int z = t / per_z, rem = t - z * per_z;
@@ -408,31 +422,36 @@ __global__ void __launch_bounds__(Cfg<BN, WG>::THREADS, 1)
       int kbeg, kend;
       krange(t, kbeg, kend);
       const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-      float acc[64];
+      float acc[32];
 #pragma unroll
-      for (int e = 0; e < 64; ++e) acc[e] = 0.f;
-      const int nch = (nkb + CK - 1) / CK;
+      for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+      const int nch = pr.noload >= 4 ? 0 : (nkb + CK - 1) / CK;  // (diagnostics: 4 = no drain)
       for (int c = 0; c < nch; ++c, ++cc) {
-        const uint32_t buf = cc & 1;
-        mbar_wait(&accf[buf], (cc >> 1) & 1);
+        const uint32_t buf = cc % C::NBUF;
+        mbar_wait(&accf[buf], (cc / C::NBUF) & 1);
         tc_fence_after();
-#pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          uint32_t rb[16], rs[16];
-          tmem_ld16(lane_base + buf * 2 * BN + (uint32_t)(p * 16), rb);
-          tmem_ld16(lane_base + buf * 2 * BN + BN + (uint32_t)(p * 16), rs);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e)
-            acc[p * 16 + e] = __fadd_rn(acc[p * 16 + e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
+        uint32_t rb[32], rs[32];
+        if (pr.noload >= 2) {  // diagnostics: release the chunk unread
+          tc_fence_before();
+          mbar_arrive(&acce[buf]);
+          continue;
         }
+        tmem_ld16(lane_base + buf * 2 * BN, rb);
+        tmem_ld16(lane_base + buf * 2 * BN + 16, rb + 16);
+        tmem_ld16(lane_base + buf * 2 * BN + BN, rs);
+        tmem_ld16(lane_base + buf * 2 * BN + BN + 16, rs + 16);
+        tmem_wait_ld();
         tc_fence_before();
-        mbar_arrive(&acce[buf]);
+        mbar_arrive(&acce[buf]);  // the registers hold the chunk: the MMA may refill the buffer
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          acc[e] = __fadd_rn(acc[e], __fadd_rn(__uint_as_float(rb[e]), __uint_as_float(rs[e])));
       }
+      if (pr.noload >= 5) continue;  // (diagnostics: 5 = no epilogue stores)
       const int i = i0 + q * 32 + (tid & 31);
       typename OUT::Row orow = out.row(z, i);
 #pragma unroll
-      for (int e = 0; e < 64; ++e) out.put(orow, j0 + cg * 64 + e, acc[e]);
+      for (int e = 0; e < 32; ++e) out.put(orow, j0 + cg * 32 + e, acc[e]);
     }
   }
   tc_fence_before();
@@ -687,6 +706,8 @@ static int launch(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMa
   const int64_t nt = (int64_t)pr.ti * pr.tj * pr.zdim;
   if (nt >= ((int64_t)1 << 31)) return PB_ERR_UNSUPPORTED;
   pr.ntiles = (int)nt;
+  static const int noload = getenv("PB_TMA_NOLOAD") ? atoi(getenv("PB_TMA_NOLOAD")) : 0;
+  pr.noload = noload;
   const int grid = (int)(nt < num_sms() ? nt : num_sms());
   tma_conv_kernel<BN, WG, OUT><<<grid, C::THREADS, C::SMEM, compute_stream()>>>(ah, al, bh, bl, pr, out);
   PB_LAUNCHED();
