@@ -164,6 +164,19 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
  * holding the kept axes in order.  Supported (else PB_ERR_UNSUPPORTED, nothing launched): 2-3
  * stages whose first two are (innermost, next) -- "rows" -- or 3 stages whose last is the
  * innermost axis -- "cols". */
+/* Windowed chain leaves: leaf l reads its source through a per-axis affine map, not a
+ * materialised pad -- for output index i, j = i*mul - off; the value is src[j / div] when j >= 0,
+ * j % div == 0 and j / div < the source extent, else `fill`.  A pad is (mul 1, off lo, div 1),
+ * a zero-stuffing pad (minml/autograd.py:667-693) div = step, a strided slice of a padded tensor
+ * mul = step.  Leaves with on == 0 broadcast as in pb_ew_chain.  Output rank <= 4. */
+typedef struct pb_leaf_window {
+  int32_t on;
+  int32_t pad_;
+  double fill;
+  int64_t mul[4], off[4], div[4]; /* per source/output axis */
+} pb_leaf_window;
+int pb_ew_chain_win(int nleaves, const pb_tensor* leaves, const pb_leaf_window* wins, int head_kind,
+                    double head_scalar, int nsteps, const pb_chain_step* steps, const pb_tensor* out);
 typedef struct pb_red_stage {
   int32_t axis;     /* source axis */
   int32_t epi_op;   /* -1 none, else PB_ADD/SUB/MUL/DIV */

@@ -844,6 +844,154 @@ static void launch_chain(ChainArgs& p, int mode, cudaStream_t s) {
   else ew_chain1<NL><<<grid_for(p.n, 256, 4), 256, 0, s>>>(p);
 }
 
+
+// windowed leaves (round 2): the reference scatters a slice's gradient back with zero-stuffing
+// pads (minml/autograd.py:667-693, the maxpool backward's 9 windows) and reads strided windows
+// of a -inf-padded input in the maxpool forward.  A windowed leaf reads its source through a
+// per-axis affine map instead of a materialised pad: for output index i, j = i*mul - off; the
+// element is src[j / div] when j >= 0, j % div == 0 and j / div < ext (the source extent), else
+// the fill value.  One thread per output element decodes its 4-D index.
+struct WinLeaf {
+  int32_t mul[4], off[4], shift[4], ext[4];  // div = 1 << shift (the host declines other divisors)
+  float fill;
+  int on;
+};
+struct WinArgs {
+  ChainArgs c;       // leaves, steps, output (c.st: broadcast strides of the plain leaves, 4-D)
+  WinLeaf w[kChainLeaves];
+  FastDiv d1, d2, d3;  // output extents of axes 1..3
+};
+
+// leaf l at 4 consecutive positions i3 .. i3+3 of the innermost axis: the outer axes' part of
+// the window test and offset is computed once per group
+__device__ __forceinline__ float4 win_load4(const WinArgs& a, int l, const uint32_t* idx) {
+  const ChainArgs& p = a.c;
+  const WinLeaf& w = a.w[l];
+  float v[4];
+  if (w.on) {
+    int64_t off = 0;
+    bool ok = true;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int j = (int)idx[d] * w.mul[d] - w.off[d];
+      const int q = j >> w.shift[d];
+      ok = ok && j >= 0 && !(j & ((1 << w.shift[d]) - 1)) && q < w.ext[d];
+      off += (int64_t)q * p.st[l][d];
+    }
+    const int m3 = (1 << w.shift[3]) - 1;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = (int)(idx[3] + u) * w.mul[3] - w.off[3];
+      const int q = j >> w.shift[3];
+      if (ok && j >= 0 && !(j & m3) && q < w.ext[3]) {
+        const int64_t o = off + (int64_t)q * p.st[l][3];
+        v[u] = p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[o] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + o);
+      } else {
+        v[u] = w.fill;
+      }
+    }
+  } else {
+    int64_t off = 0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) off += (int64_t)idx[d] * p.st[l][d];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t o = off + (int64_t)(idx[3] + u) * p.st[l][3];
+      v[u] = p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[o] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + o);
+    }
+  }
+  return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+__device__ __forceinline__ float win_load1(const WinArgs& a, int l, const uint32_t* idx) {
+  const ChainArgs& p = a.c;
+  const WinLeaf& w = a.w[l];
+  int64_t off = 0;
+  if (w.on) {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const int j = (int)idx[d] * w.mul[d] - w.off[d];
+      if (j < 0 || (j & ((1 << w.shift[d]) - 1))) return w.fill;
+      const int q = j >> w.shift[d];
+      if (q >= w.ext[d]) return w.fill;
+      off += (int64_t)q * p.st[l][d];
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < 4; ++d) off += (int64_t)idx[d] * p.st[l][d];
+  }
+  return p.is_bool[l] ? (((const uint8_t*)p.leaf[l])[off] ? 1.f : 0.f) : __ldg((const float*)p.leaf[l] + off);
+}
+
+// one output per thread-iteration (inner extents that are not a multiple of 4)
+template <int NL>
+__global__ void __launch_bounds__(256) ew_chain_win1(WinArgs a) {
+  const ChainArgs& p = a.c;
+  const uint32_t step = gridDim.x * blockDim.x;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < p.n; e += step) {
+    uint32_t idx[4], q;
+    a.d3.divmod(e, q, idx[3]);
+    a.d2.divmod(q, q, idx[2]);
+    a.d1.divmod(q, idx[0], idx[1]);
+    const float x0 = win_load1(a, 0, idx);
+    const float x1 = NL > 1 ? win_load1(a, NL > 1 ? 1 : 0, idx) : 0.f;
+    const float x2 = NL > 2 ? win_load1(a, NL > 2 ? 2 : 0, idx) : 0.f;
+    const float x3 = NL > 3 ? win_load1(a, NL > 3 ? 3 : 0, idx) : 0.f;
+    const float x4 = NL > 4 ? win_load1(a, NL > 4 ? 4 : 0, idx) : 0.f;
+    const float x5 = NL > 5 ? win_load1(a, NL > 5 ? 5 : 0, idx) : 0.f;
+    const float x6 = NL > 6 ? win_load1(a, NL > 6 ? 6 : 0, idx) : 0.f;
+    const float x7 = NL > 7 ? win_load1(a, NL > 7 ? 7 : 0, idx) : 0.f;
+    float v = p.head_kind == 0 ? x0 : p.head_scalar;
+    for (int s = 0; s < p.nsteps; ++s) {
+      const ChainStep st = p.step[s];
+      float o = v;
+      if (st.kind == 1) o = pick<NL>(st.leaf, x0, x1, x2, x3, x4, x5, x6, x7);
+      else if (st.kind == 2) o = st.scalar;
+      const float4 r = chain_step4(st, make_float4(v, v, v, v), make_float4(o, o, o, o));
+      v = r.x;
+    }
+    if (p.out_bool)
+      ((uint8_t*)p.out)[e] = v != 0.f;
+    else
+      ((float*)p.out)[e] = v;
+  }
+}
+
+// 4 consecutive outputs along the innermost axis per thread-iteration (its extent % 4 == 0)
+template <int NL>
+__global__ void __launch_bounds__(256) ew_chain_win(WinArgs a) {
+  const ChainArgs& p = a.c;
+  const uint32_t step = gridDim.x * blockDim.x;
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < p.n; g += step) {
+    const uint32_t e = g * 4u;
+    uint32_t idx[4], q;
+    a.d3.divmod(e, q, idx[3]);
+    a.d2.divmod(q, q, idx[2]);
+    a.d1.divmod(q, idx[0], idx[1]);
+    const float4 x0 = win_load4(a, 0, idx);
+    const float4 x1 = NL > 1 ? win_load4(a, NL > 1 ? 1 : 0, idx) : z;
+    const float4 x2 = NL > 2 ? win_load4(a, NL > 2 ? 2 : 0, idx) : z;
+    const float4 x3 = NL > 3 ? win_load4(a, NL > 3 ? 3 : 0, idx) : z;
+    const float4 x4 = NL > 4 ? win_load4(a, NL > 4 ? 4 : 0, idx) : z;
+    const float4 x5 = NL > 5 ? win_load4(a, NL > 5 ? 5 : 0, idx) : z;
+    const float4 x6 = NL > 6 ? win_load4(a, NL > 6 ? 6 : 0, idx) : z;
+    const float4 x7 = NL > 7 ? win_load4(a, NL > 7 ? 7 : 0, idx) : z;
+    float4 v = p.head_kind == 0 ? x0 : make_float4(p.head_scalar, p.head_scalar, p.head_scalar, p.head_scalar);
+    for (int s = 0; s < p.nsteps; ++s) {
+      const ChainStep st = p.step[s];
+      float4 o = v;
+      if (st.kind == 1) o = pick<NL>(st.leaf, x0, x1, x2, x3, x4, x5, x6, x7);
+      else if (st.kind == 2) o = make_float4(st.scalar, st.scalar, st.scalar, st.scalar);
+      v = chain_step4(st, v, o);
+    }
+    if (p.out_bool)
+      reinterpret_cast<uchar4*>(p.out)[g] = make_uchar4(v.x != 0.f, v.y != 0.f, v.z != 0.f, v.w != 0.f);
+    else
+      reinterpret_cast<float4*>(p.out)[g] = v;
+  }
+}
+
 // ----------------------------------------------------------------------- host helpers
 static void fill_dims(Dims& d, const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
   d.ndim = out->ndim;
@@ -1370,6 +1518,7 @@ __device__ __forceinline__ void rc_eval_batch(const RCArgs& p, const int64_t (&o
   float4 x[NL][B];
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
+    if (l >= p.nleaves) continue;  // NL is a bucket (1, 2, 3, 4, 8): leaves past nleaves are never read
     const bool vec = V4 && p.s_vec[l];
     if (p.is_bool[l]) {
       const uint8_t* b8 = (const uint8_t*)p.leaf[l];
@@ -2118,6 +2267,96 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
     case 4: launch_redchain<4, false>(p, rows, v4, (int)grid, threads, smem, s); break;
     default: launch_redchain<8, false>(p, rows, v4, (int)grid, threads, smem, s); break;
   }
+  PB_LAUNCHED();
+  return PB_OK;
+}
+
+
+int pb_ew_chain_win(int nleaves, const pb_tensor* leaves, const pb_leaf_window* wins, int head_kind,
+                    double head_scalar, int nsteps, const pb_chain_step* steps, const pb_tensor* out) {
+  const int64_t n = numel(*out);
+  if (n == 0) return PB_OK;
+  if (nleaves < 1 || nleaves > kChainLeaves || nsteps < 0 || nsteps > kChainSteps)
+    return fail(PB_ERR_ARG, "pb_ew_chain_win: bad chain shape");
+  if (n >= ((int64_t)1 << 31) || !is_contiguous(*out) || (out->dtype != PB_F32 && out->dtype != PB_BOOL) ||
+      out->ndim > 4 || out->ndim < 1)
+    return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain_win: output must be a dense f32/bool tensor of rank <= 4");
+  const bool vec = out->shape[out->ndim - 1] % 4 == 0 && (out->ptr & 15) == 0;
+  WinArgs a;
+  memset(&a, 0, sizeof(a));
+  ChainArgs& p = a.c;
+  p.nleaves = nleaves;
+  p.nsteps = nsteps;
+  p.head_kind = head_kind;
+  p.head_scalar = (float)head_scalar;
+  p.out = (void*)(uintptr_t)out->ptr;
+  p.out_bool = out->dtype == PB_BOOL;
+  p.n = (uint32_t)(vec ? n / 4 : n);
+  for (int k = 0; k < nsteps; ++k) {
+    const pb_chain_step& c = steps[k];
+    if (c.kind == 1 && (c.leaf < 0 || c.leaf >= nleaves)) return fail(PB_ERR_ARG, "pb_ew_chain_win: bad leaf index");
+    p.step[k].op = (int16_t)c.op;
+    p.step[k].kind = (int8_t)c.kind;
+    p.step[k].side = (int8_t)c.side;
+    p.step[k].leaf = (int8_t)c.leaf;
+    p.step[k].to_bool = (int8_t)c.to_bool;
+    p.step[k].scalar = (float)c.scalar;
+  }
+  const int pad = 4 - out->ndim;
+  int64_t oshape[4];
+  for (int d = 0; d < 4; ++d) oshape[d] = d < pad ? 1 : out->shape[d - pad];
+  for (int l = 0; l < nleaves; ++l) {
+    const pb_tensor& t = leaves[l];
+    if (t.dtype != PB_F32 && t.dtype != PB_BOOL) return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain_win: leaf dtype");
+    p.leaf[l] = (const void*)(uintptr_t)t.ptr;
+    p.is_bool[l] = t.dtype == PB_BOOL;
+    const int off = 4 - t.ndim;
+    if (off < 0) return fail(PB_ERR_ARG, "pb_ew_chain_win: leaf rank exceeds 4");
+    for (int d = 0; d < 4; ++d) p.st[l][d] = 0;
+    WinLeaf& w = a.w[l];
+    w.on = wins && wins[l].on;
+    if (w.on) {
+      if (t.ndim != out->ndim) return fail(PB_ERR_ARG, "pb_ew_chain_win: a windowed leaf has the output's rank");
+      w.fill = (float)wins[l].fill;
+      for (int d = 0; d < 4; ++d) {
+        const int k = d - pad;
+        const int64_t mul = k < 0 ? 1 : wins[l].mul[k], dv = k < 0 ? 1 : wins[l].div[k];
+        const int64_t wo = k < 0 ? 0 : wins[l].off[k], ext = k < 0 ? 1 : t.shape[k];
+        if (dv < 1 || (dv & (dv - 1))) return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain_win: window divisor not 2^k");
+        // 32-bit index math: |i*mul - off| must fit
+        if (mul < 0 || mul * oshape[d] + (wo < 0 ? -wo : wo) >= ((int64_t)1 << 30) || ext >= ((int64_t)1 << 30))
+          return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain_win: window coordinates exceed 32 bits");
+        int sh = 0;
+        while (((int64_t)1 << sh) < dv) ++sh;
+        w.mul[d] = (int32_t)mul;
+        w.off[d] = (int32_t)wo;
+        w.shift[d] = sh;
+        w.ext[d] = (int32_t)ext;
+        p.st[l][d] = k < 0 ? 0 : t.strides[k];
+      }
+    } else {
+      for (int k = 0; k < t.ndim; ++k) p.st[l][off + k] = t.shape[k] == 1 ? 0 : t.strides[k];
+    }
+  }
+  a.d1 = FastDiv((uint32_t)oshape[1]);
+  a.d2 = FastDiv((uint32_t)oshape[2]);
+  a.d3 = FastDiv((uint32_t)oshape[3]);
+  cudaStream_t s = compute_stream();
+  const int grid = grid_for(p.n, 256, 2);
+#define PB_WIN(K)                                              \
+  if (vec) ew_chain_win<K><<<grid, 256, 0, s>>>(a);            \
+  else ew_chain_win1<K><<<grid, 256, 0, s>>>(a);
+  switch (nleaves) {
+    case 1: PB_WIN(1) break;
+    case 2: PB_WIN(2) break;
+    case 3: PB_WIN(3) break;
+    case 4: PB_WIN(4) break;
+    case 5: PB_WIN(5) break;
+    case 6: PB_WIN(6) break;
+    case 7: PB_WIN(7) break;
+    default: PB_WIN(8) break;
+  }
+#undef PB_WIN
   PB_LAUNCHED();
   return PB_OK;
 }

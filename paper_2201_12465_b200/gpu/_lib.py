@@ -21,6 +21,7 @@ SCALAR = struct.Struct("<iidq")      # pb_scalar: kind, pad, f, i
 CONV = struct.Struct("<iiii")        # pb_conv
 STEP = struct.Struct("<iiiiiid")     # pb_chain_step: op, kind, side, leaf, to_bool, pad, scalar
 RSTAGE = struct.Struct("<iiif")      # pb_red_stage: axis, epi_op, epi_left, scalar
+WINDOW = struct.Struct("<iid4q4q4q")  # pb_leaf_window: on, pad, fill, mul[4], off[4], div[4]
 _ZEROS = (0,) * MAX_RANK
 
 BINOP = {"add": 0, "sub": 1, "mul": 2, "div": 3, "pow": 4, "minimum": 5, "maximum": 6, "eq": 7,
@@ -102,6 +103,7 @@ SIGNATURES = {
     "pb_conv2d_grad_weight": (_I, [_B, _B, _B, _B]),
     "pb_ew_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _B]),
     "pb_reduce_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _I, _B, _I, _B, _B]),
+    "pb_ew_chain_win": (_I, [_I, _B, _B, _I, ctypes.c_double, _I, _B, _B]),
     "pb_sgd": (_I, [_I, _U64P, _U64P, _U64P, _U64P, _U64P, _I64P, _F, _F, _F]),
     "pb_bucket_pack": (_I, [_I, _U64P, _I64P, _U64]),
     "pb_scale_f32": (_I, [_U64, ctypes.c_int64, _F]),

@@ -259,7 +259,64 @@ class LazyReduce:
         return self.dev().packed()
 
 
+class LazyWindow:
+    """Adapter of a deferred pad / zero-stuffing / strided slice of a device array (backend-
+    internal fusion, round 2): element i of axis d is src[j / div] for j = i*mul - off when
+    j >= 0, j % div == 0 and j / div < src.shape[d], else ``fill``.  The reference's slice
+    backward scatters with zero-stuffing pads (minml/autograd.py:667-693) and its maxpool reads
+    strided windows of a -inf-padded input; chain kernels read such a leaf through the map
+    (``pb_ew_chain_win``) instead of materialising the padded tensor.  Any other use
+    materialises it once, with the same values the eager pad would write."""
+
+    __slots__ = ("be", "src", "shape", "strides", "dtype", "host", "win", "fill", "_dev", "__weakref__")
+
+    def __init__(self, be, src, shape, win, fill):
+        self.be, self.src, self.win, self.fill = be, src, tuple(win), float(fill)
+        self.shape = tuple(shape)
+        self.strides = contig_strides(self.shape)
+        self.dtype = src.dtype
+        self.host = None
+        self._dev = None
+
+    def dev(self):
+        d = self._dev
+        if d is None:
+            d = self._dev = self.be._run_window(self)
+        return d
+
+    def materialize(self):
+        self.dev()
+
+    @property
+    def block(self):
+        return self.dev().block
+
+    @property
+    def ptr(self):
+        return self.dev().ptr
+
+    @property
+    def contiguous(self):
+        return True
+
+    def packed(self):
+        return self.dev().packed()
+
+    def window_bytes(self):
+        r = len(self.shape)
+        mul = [w[0] for w in self.win] + [1] * (4 - r)
+        off = [w[1] for w in self.win] + [0] * (4 - r)
+        div = [w[2] for w in self.win] + [1] * (4 - r)
+        return _lib.WINDOW.pack(1, 0, self.fill, *mul, *off, *div)
+
+
+_LAZY = (LazyArray, LazyReduce, LazyWindow)
+_CHAINABLE = (LazyArray, LazyWindow)
+_NO_WINDOW = _lib.WINDOW.pack(0, 0, 0.0, *([0] * 12)) if hasattr(_lib, "WINDOW") else b""
+
+
 _EPI = {"add", "sub", "mul", "div"}
+_WINDOW_OPS = {"pad", "reshape", "slice"}
 
 
 class GraphExec:
@@ -405,7 +462,7 @@ class GpuBackend(Backend):
         return DeviceArray(blk, blk.ptr, shape, contig_strides(shape), dt)
 
     def _contig(self, a, opname="materialize"):
-        if type(a) is LazyArray:
+        if type(a) in _LAZY:
             return a.dev()
         if a.contiguous:
             return a
@@ -430,8 +487,12 @@ class GpuBackend(Backend):
         name = call.name
         if name == "sum":
             pass  # _reduce extends or runs lazy sources itself
-        elif name not in _FUSE_BIN and name not in _FUSE_UN:
+        elif name == "slice":  # windows and chains compose with a slice (pushed into the leaves)
+            args = [a.dev() if type(a) is LazyReduce else a for a in args]
+        elif name in _WINDOW_OPS:  # a LazyWindow source composes; other lazies run first
             args = [a.dev() if type(a) is LazyArray or type(a) is LazyReduce else a for a in args]
+        elif name not in _FUSE_BIN and name not in _FUSE_UN:
+            args = [a.dev() if type(a) in _LAZY else a for a in args]
         elif type(args[0]) is LazyReduce and not (name in _EPI and "scalar" in call.params):
             args = [a.dev() if type(a) is LazyReduce else a for a in args]
         elif len(args) > 1 and type(args[1]) is LazyReduce:
@@ -458,6 +519,7 @@ class GpuBackend(Backend):
         sig = (name, tuple(call.shape), call.dtype.name, tuple(tuple(a.shape) for a in args))
         prods = tuple(self._producer(a) for a in args)
         if self._trace is not None:
+            fusible = fusible or name == "slice"  # a slice of a lazy chain is pushed into its leaves
             epi = name in _EPI and "scalar" in call.params and call.dtype is dtypes.f32
             red_ax = name == "sum" and call.dtype is dtypes.f32 and call.params.get("axis") is not None
             self._trace.append((sig, prods, fusible, epi, red_ax))
@@ -470,7 +532,7 @@ class GpuBackend(Backend):
             else:  # the step diverged from the trace: stop fusing (everything materialises)
                 self._abandon_plan()
         res = self._execute(call, args)
-        if type(res) is DeviceArray or type(res) is LazyArray or type(res) is LazyReduce:
+        if type(res) is DeviceArray or type(res) in _LAZY:
             self._prod[id(res)] = (idx, weakref.ref(res))
         return res
 
@@ -796,10 +858,17 @@ class GpuBackend(Backend):
         leaves.append(d)
         return len(leaves) - 1
 
+    @staticmethod
+    def _window_fit(call, args):
+        """Windowed leaves enter a chain only at the output's exact shape (no broadcasting)."""
+        shape = tuple(call.shape)
+        return [a.dev() if type(a) is LazyWindow and (a.shape != shape or len(shape) > 4) else a for a in args]
+
     def _try_fuse_binary(self, call, args):
         name = call.name
         p = call.params
         out_dt = call.dtype
+        args = self._window_fit(call, args)
         if not self._fuse or len(call.shape) > 4 or (out_dt is not dtypes.f32 and out_dt is not dtypes.bool_):
             return None
         code = _lib.BINOP[name]
@@ -843,6 +912,7 @@ class GpuBackend(Backend):
 
     def _try_fuse_unary(self, call, args):
         name = call.name
+        args = self._window_fit(call, args)
         a = args[0]
         out_dt = call.dtype
         if not self._fuse or len(call.shape) > 4 or not self._fusible_operand(a):
@@ -867,9 +937,20 @@ class GpuBackend(Backend):
         out = self._new(lz.shape, lz.dtype, "fused")
         if out.block is None:
             return out
-        leaves = b"".join(d.packed() for d in lz.leaves)
         steps = b"".join(_lib.STEP.pack(op, kind, side, leaf, tb, 0, sc) for op, kind, side, leaf, tb, sc in lz.steps)
         hk, hv = (0, 0.0) if lz.head[0] == "leaf" else (1, float(lz.head[1]))
+        if any(type(d) is LazyWindow and d._dev is None for d in lz.leaves):
+            leaves = b"".join(d.src.packed() if type(d) is LazyWindow and d._dev is None else d.packed()
+                              for d in lz.leaves)
+            wins = b"".join(d.window_bytes() if type(d) is LazyWindow and d._dev is None else _NO_WINDOW
+                            for d in lz.leaves)
+            rc = self._lib.pb_ew_chain_win(len(lz.leaves), leaves, wins, hk, hv, len(lz.steps), steps, out.packed())
+            if rc != _lib.UNSUPPORTED:
+                _lib.check(rc, "fused windowed chain")
+                return out
+            # the kernel declined a window (divisor not a power of two, > 32-bit coordinates):
+            # materialise the windowed leaves and run the plain chain
+        leaves = b"".join(d.packed() for d in lz.leaves)
         _lib.check(self._lib.pb_ew_chain(len(lz.leaves), leaves, hk, hv, len(lz.steps), steps, out.packed()),
                    "fused elementwise chain")
         return out
@@ -892,12 +973,12 @@ class GpuBackend(Backend):
             view = self._times_one(call, args)
             if view is not None:
                 return view
-        if self._fuse and (self._lazy_ok or type(args[0]) is LazyArray or
-                           (len(args) > 1 and type(args[1]) is LazyArray)):
+        if self._fuse and (self._lazy_ok or type(args[0]) in _CHAINABLE or
+                           (len(args) > 1 and type(args[1]) in _CHAINABLE)):
             lz = self._try_fuse_binary(call, args)
             if lz is not None:
                 return lz if self._lazy_ok else lz.dev()
-            args = [a.dev() if type(a) is LazyArray else a for a in args]
+        args = [a.dev() if type(a) in _CHAINABLE else a for a in args]
         out = self._new(tuple(call.shape), call.dtype, name)
         if out.block is None:
             return out
@@ -968,11 +1049,11 @@ class GpuBackend(Backend):
             raise DomainError(msg)
 
     def _unary(self, call, args):
-        if self._fuse and (self._lazy_ok or type(args[0]) is LazyArray):
+        if self._fuse and (self._lazy_ok or type(args[0]) in _CHAINABLE):
             lz = self._try_fuse_unary(call, args)
             if lz is not None:
                 return lz if self._lazy_ok else lz.dev()
-            args = [a.dev() if type(a) is LazyArray else a for a in args]
+        args = [a.dev() if type(a) in _CHAINABLE else a for a in args]
         a = args[0]
         out = self._new(tuple(call.shape), call.dtype, call.name)
         if out.block is None:
@@ -984,6 +1065,8 @@ class GpuBackend(Backend):
     # reductions
     def _reduce(self, call, args):
         a = args[0]
+        if type(a) is LazyWindow:
+            a = a.dev()
         if type(a) is LazyReduce:
             nl = a.extend(call) if call.shape.size > 0 else None
             if nl is None:
@@ -1093,6 +1176,11 @@ class GpuBackend(Backend):
     def _reshape(self, call, args):
         a = args[0]
         shape = tuple(call.shape)
+        if type(a) is LazyWindow:
+            lw = self._window_reshape(a, shape)
+            if lw is not None:
+                return lw
+            a = a.dev()
         if not a.contiguous:
             a = self._contig(a, "reshape")
         return DeviceArray(a.block, a.ptr, shape, contig_strides(shape), a.dtype, a.host.reshape(shape)
@@ -1107,6 +1195,16 @@ class GpuBackend(Backend):
     def _slice(self, call, args):
         a = args[0]
         p = call.params
+        if type(a) is LazyWindow:  # i = start + i' * step  ->  mul' = mul*step, off' = off - start*mul
+            win = tuple((m * st, o - s0 * m, dv) for (m, o, dv), s0, st in zip(a.win, p["starts"], p["steps"]))
+            return LazyWindow(self, a.src, tuple(call.shape), win, a.fill)
+        if type(a) is LazyArray:
+            if self._fuse and a._dev is None and 0 not in tuple(call.shape):
+                # elementwise ops commute with slicing: slice every leaf instead of the result
+                leaves = tuple(self._slice_leaf(d, a.shape, p["starts"], p["steps"], tuple(call.shape))
+                               for d in a.leaves)
+                return LazyArray(self, tuple(call.shape), a.dtype, leaves, a.head, a.steps)
+            a = a.dev()
         off = 0
         for st, s in zip(p["starts"], a.strides):
             off += st * s
@@ -1133,12 +1231,97 @@ class GpuBackend(Backend):
 
     def _pad(self, call, args):
         a = args[0]
+        value = call.params.get("value", 0)
+        pw = call.params["pad_width"]
+        if self._fuse and (type(a) is LazyWindow or (type(a) is DeviceArray and a.block is not None)) and \
+                len(a.shape) == len(pw) and (a.dtype is dtypes.f32 or a.dtype is dtypes.bool_) and \
+                type(value) in (int, float, bool):
+            fill = float(bool(value)) if a.dtype is dtypes.bool_ else float(np.float32(value))
+            if fill != 0.0 and type(a) is DeviceArray:
+                # a -inf / constant border (the maxpool forward): its 9 strided windows read the
+                # materialised pad faster than the per-element window decode (measured)
+                return self._pad_now(call, a, value)
+            if type(a) is DeviceArray:
+                return LazyWindow(self, a, tuple(call.shape), tuple((1, lo, 1) for lo, _ in pw), fill)
+            if a.fill == fill or (fill != fill and a.fill != a.fill):  # one fill value (NaN == NaN)
+                win = tuple((m, o + lo * m, dv) for (m, o, dv), (lo, _) in zip(a.win, pw))
+                return LazyWindow(self, a.src, tuple(call.shape), win, fill)
+            a = a.dev()
+        elif type(a) is LazyWindow:
+            a = a.dev()
+        return self._pad_now(call, a, value)
+
+    def _pad_now(self, call, a, value):
         out = self._new(tuple(call.shape), call.dtype, "pad")
         if out.block is None:
             return out
         lo = (ctypes.c_int64 * 8)(*[lo for lo, _ in call.params["pad_width"]])
-        _lib.check(self._lib.pb_pad(a.packed(), lo, _lib.pack_scalar(call.params.get("value", 0)), out.packed()),
-                   "pad")
+        _lib.check(self._lib.pb_pad(a.packed(), lo, _lib.pack_scalar(value), out.packed()), "pad")
+        return out
+
+    def _slice_leaf(self, d, full, starts, steps, out_shape):
+        """Chain leaf d (broadcast to `full`) restricted to the slice that produced `out_shape`."""
+        if type(d) is LazyWindow:  # windowed leaves have the chain's full shape
+            win = tuple((m * st, o - s0 * m, dv) for (m, o, dv), s0, st in zip(d.win, starts, steps))
+            return LazyWindow(self, d.src, out_shape, win, d.fill)
+        r, R = len(d.shape), len(full)
+        ptr, shape, strides = d.ptr, list(d.shape), list(d.strides)
+        for k in range(R):
+            kk = k - (R - r)
+            if kk < 0 or d.shape[kk] == 1:
+                continue  # broadcast axis: unchanged
+            ptr += starts[k] * d.strides[kk] * d.dtype.itemsize
+            strides[kk] = d.strides[kk] * steps[k]
+            shape[kk] = out_shape[k]
+        return DeviceArray(d.block, ptr, tuple(shape), tuple(strides), d.dtype)
+
+    def _window_reshape(self, a, shape):
+        """The reshapes _slice_grad applies to a windowed tensor: insert one unit axis, or merge an
+        axis with a following zero-stuffing axis (source extent 1 at index 0): (a, b) -> a*k + b
+        with only b == 0 populated is div' = k*div, off' = k*off.  None: materialise instead."""
+        old = a.shape
+        src = a.src
+        if len(shape) == len(old) + 1:
+            for p in range(len(shape)):
+                if shape[p] == 1 and shape[:p] + shape[p + 1:] == old:
+                    s2 = DeviceArray(src.block, src.ptr, src.shape[:p] + (1,) + src.shape[p:],
+                                     src.strides[:p] + (0,) + src.strides[p:], src.dtype)
+                    return LazyWindow(self, s2, shape, a.win[:p] + ((1, 0, 1),) + a.win[p:], a.fill)
+            return None
+        if len(shape) == len(old) - 1:
+            for p in range(len(old) - 1):
+                k = old[p + 1]
+                if old[:p] + (old[p] * k,) + old[p + 2:] != shape:
+                    continue
+                mb, ob, db = a.win[p + 1]
+                ma, oa, da = a.win[p]
+                if src.shape[p + 1] == 1 and (mb, ob, db) == (1, 0, 1) and ma == 1:
+                    s2 = DeviceArray(src.block, src.ptr, src.shape[:p + 1] + src.shape[p + 2:],
+                                     src.strides[:p + 1] + src.strides[p + 2:], src.dtype)
+                    win = a.win[:p] + ((1, k * oa, k * da),) + a.win[p + 2:]
+                    return LazyWindow(self, s2, shape, win, a.fill)
+            return None
+        return None
+
+    def _run_window(self, lw):
+        """Materialise a LazyWindow with the values the eager pad would have written."""
+        out = self._new(lw.shape, lw.dtype, "pad")
+        if out.block is None:
+            return out
+        src = lw.src
+        if all(m == 1 and o >= 0 for m, o, _ in lw.win):  # a pad / zero-stuffing: fill, then a strided copy
+            _lib.check(self._lib.pb_fill(out.packed(), _lib.pack_scalar(bool(lw.fill) if lw.dtype is dtypes.bool_
+                                                                         else lw.fill)), "pad fill")
+            off = sum(o * st for (_, o, _), st in zip(lw.win, out.strides))
+            dst = DeviceArray(out.block, out.ptr + off * out.dtype.itemsize, src.shape,
+                              tuple(dv * st for (_, _, dv), st in zip(lw.win, out.strides)), out.dtype)
+            if src.shape and 0 not in src.shape:
+                _lib.check(self._lib.pb_copy(src.packed(), dst.packed()), "pad copy")
+            return out
+        if len(lw.shape) > 4:
+            raise DeviceError(f"windowed tensor of rank {len(lw.shape)} cannot be materialised by the chain kernel")
+        _lib.check(self._lib.pb_ew_chain_win(1, src.packed(), lw.window_bytes(), 0, 0.0, 0, b"", out.packed()),
+                   "windowed materialisation")
         return out
 
     # -------------------------------------------------------------- collectives
