@@ -694,7 +694,7 @@ static int run(const LA& la, const LB& lb, const OUT& out, int Mi, int Nj, int K
   OutPartial part{ws_after, Mi, Nj};
   int rc = launch<BN>(la, lb, part, Mi, Nj, K, splits, kper, 0);
   if (rc) return rc;
-  fold_partials<OUT><<<grid_for((int64_t)Mi * Nj, 256), 256, 0, compute_stream()>>>(ws_after, splits, Mi, Nj, out);
+  launch_fold<OUT>(ws_after, splits, Mi, Nj, out, compute_stream());
   PB_LAUNCHED();
   return PB_OK;
 }

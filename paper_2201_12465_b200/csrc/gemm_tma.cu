@@ -788,8 +788,7 @@ static int run_conv(Prob& pr, const float* xh, const float* xl, const float* wh,
     OutPartial op{pw, pr.Mi, pr.Nj};
     int rc = BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, op) : launch<128, false>(ah, al, bh, bl, pr, op);
     if (rc) return rc;
-    fold_partials<OUT><<<grid_for((int64_t)pr.Mi * pr.Nj, 256), 256, 0, compute_stream()>>>(pw, pr.zdim, pr.Mi,
-                                                                                             pr.Nj, o);
+    launch_fold<OUT>(pw, pr.zdim, pr.Mi, pr.Nj, o, compute_stream());
     PB_LAUNCHED();
     return PB_OK;
   }
@@ -1122,7 +1121,7 @@ int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* gr, const pb_
   int rc = BN == 64 ? launch<64, true>(ah, al, bh, bl, pr, o) : launch<128, true>(ah, al, bh, bl, pr, o);
   if (rc || splits == 1) return rc;
   OutMat fin{dw, C * RS, F, (int64_t)C * RS, 0};
-  fold_partials<OutMat><<<grid_for((int64_t)C * RS * F, 256), 256, 0, compute_stream()>>>(part, splits, C * RS, F, fin);
+  launch_fold<OutMat>(part, splits, C * RS, F, fin, compute_stream());
   PB_LAUNCHED();
   return PB_OK;
 }
@@ -1230,10 +1229,10 @@ int pb_conv2d_grad_weight_mm(const pb_tensor* x, const pb_tensor* gr, const pb_c
   if (rc) return rc;
   if (swap) {
     OutRows fin{dw, (int)Mi, (int)Nj, C};
-    fold_partials<OutRows><<<grid_for(Mi * Nj, 256), 256, 0, s>>>(pw, splits, (int)Mi, (int)Nj, fin);
+    launch_fold<OutRows>(pw, splits, (int)Mi, (int)Nj, fin, s);
   } else {
     OutMat fin{dw, (int)Mi, (int)Nj, C, 0};
-    fold_partials<OutMat><<<grid_for(Mi * Nj, 256), 256, 0, s>>>(pw, splits, (int)Mi, (int)Nj, fin);
+    launch_fold<OutMat>(pw, splits, (int)Mi, (int)Nj, fin, s);
   }
   PB_LAUNCHED();
   return PB_OK;
@@ -1300,7 +1299,7 @@ int pb_matmul_tma(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) 
   int rc = BN == 64 ? launch<64, false>(ah, al, bh, bl, pr, op) : launch<128, false>(ah, al, bh, bl, pr, op);
   if (rc) return rc;
   OutMat fin{c, (int)N, (int)M, N, 0};
-  fold_partials<OutMat><<<grid_for(M * N, 256), 256, 0, s>>>(pw, splits, (int)N, (int)M, fin);
+  launch_fold<OutMat>(pw, splits, (int)N, (int)M, fin, s);
   PB_LAUNCHED();
   return PB_OK;
 }

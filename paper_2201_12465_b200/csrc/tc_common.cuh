@@ -174,16 +174,59 @@ struct OutPartial {  // ws[split][j][i] (fold_partials finishes through the real
   }
 };
 
-// fold split-K partials ws[split][j][i] in split order and store through OUT
+// fold split-K partials ws[split][j][i] in split order (f64) and store through OUT.  A thread
+// owns V consecutive i of one j (float4 loads when Mi % 4 == 0); all splits' loads are issued
+// before the f64 adds, and the (i, j) decode is one 32-bit FastDiv.
+template <class OUT, int V>
+__global__ void __launch_bounds__(256) fold_partials(const float* __restrict__ ws, int splits, int Mi, int Nj,
+                                                     FastDiv fMv, OUT out) {
+  const uint32_t MN = (uint32_t)Mi * (uint32_t)Nj, units = MN / V;
+  for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < units; u += gridDim.x * blockDim.x) {
+    uint32_t j, iv;
+    fMv.divmod(u, j, iv);  // fMv divides by Mi / V
+    const uint32_t idx = u * V;
+    double a[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) a[e] = 0.0;
+    int s = 0;
+    for (; s + 4 <= splits; s += 4) {
+      float v[4][V];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float* src = ws + (size_t)(s + k) * MN + idx;
+        if (V == 4) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+          v[k][0] = t.x;
+          v[k][V > 1 ? 1 : 0] = t.y;
+          v[k][V > 2 ? 2 : 0] = t.z;
+          v[k][V > 3 ? 3 : 0] = t.w;
+        } else {
+          v[k][0] = __ldg(src);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int e = 0; e < V; ++e) a[e] += (double)v[k][e];
+    }
+    for (; s < splits; ++s) {
+      const float* src = ws + (size_t)s * MN + idx;
+#pragma unroll
+      for (int e = 0; e < V; ++e) a[e] += (double)__ldg(src + e);
+    }
+#pragma unroll
+    for (int e = 0; e < V; ++e) out.put(out.row(0, (int)(iv * V + e)), (int)j, (float)a[e]);
+  }
+}
+
+// launch the fold (the partials of split 0 start the sum: v = ws[0] + ws[1] + ... in split order)
 template <class OUT>
-__global__ void fold_partials(const float* ws, int splits, int Mi, int Nj, OUT out) {
-  int64_t MN = (int64_t)Mi * Nj;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < MN;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    double v = ws[idx];  // f64: the long-K split sums (wgrad over N*Ho*Wo) add up ~148 partials
-    for (int s = 1; s < splits; ++s) v += (double)ws[(int64_t)s * MN + idx];
-    int j = (int)(idx / Mi), i = (int)(idx - (int64_t)j * Mi);
-    out.put(out.row(0, i), j, (float)v);
+inline void launch_fold(const float* ws, int splits, int Mi, int Nj, const OUT& out, cudaStream_t st) {
+  const int64_t MN = (int64_t)Mi * Nj;
+  if (Mi % 4 == 0 && ((uintptr_t)ws & 15) == 0) {
+    fold_partials<OUT, 4><<<grid_for(MN / 4, 256), 256, 0, st>>>(ws, splits, Mi, Nj, FastDiv((uint32_t)(Mi / 4)), out);
+  } else {
+    fold_partials<OUT, 1><<<grid_for(MN, 256), 256, 0, st>>>(ws, splits, Mi, Nj, FastDiv((uint32_t)Mi), out);
   }
 }
 
