@@ -156,6 +156,10 @@ typedef struct pb_chain_step {
 } pb_chain_step;
 int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
                 const pb_chain_step* steps, const pb_tensor* out);
+/* Chain kernels specialised per structure with NVRTC (straight-line code, the same functors and
+ * flags as the interpreter: bit-identical); this returns how many are compiled and cached, or -1
+ * when the JIT is off (PB_CHAIN_JIT=0 or libnvrtc missing: the interpreter runs every chain). */
+int pb_chain_jit_kernels(void);
 /* Fused multi-stage f32 sum over an elementwise chain (minml/nn.py:288-306
  * BatchNorm's x.mean(3).mean(2).mean(0) and minml/autograd.py:290-297 _unbroadcast's
  * sum(0).sum(2).sum(3)): the source is the chain above evaluated over src_shape (a plain tensor

@@ -52,7 +52,7 @@ def build(verbose=False):
     if os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(o) for o in objs):
         return OUT
     tmp = OUT + f".tmp{os.getpid()}"
-    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lnccl", "-lcudart"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lnccl", "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -18,6 +18,11 @@
 #include <vector>
 #include <cstring>
 #include <cstdlib>
+#include <cuda.h>
+#include <dlfcn.h>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 #include "common.cuh"
 
 namespace pb {
@@ -992,6 +997,275 @@ __global__ void __launch_bounds__(256) ew_chain_win(WinArgs a) {
   }
 }
 
+
+// ------------------------------------------------------------ JIT-specialised chain kernels
+// The interpreted chain kernels dispatch every step through a switch: ~68 instructions per
+// element for a 3-step chain (ncu: issue-bound at 2.4 IPC, DRAM 41%).  A chain's structure --
+// rank, vector width, leaf kinds, the op sequence -- is fixed per call site, so it is compiled
+// once with NVRTC (dlopen'd; -fmad=false, the same libdevice and IEEE division as this file) into
+// a straight-line kernel and cached by its source text.  Scalars and pointers stay parameters,
+// so every instance of a structure shares one kernel.  The functors below are the exact
+// expressions of Bin / Un / div_ieee above: results are bit-identical to the interpreter
+// (tests/test_gpu_fusion.py).  Disabled with PB_CHAIN_JIT=0, and on any NVRTC failure.
+struct JFD {
+  uint32_t d, m, s;
+};
+struct JArgs {
+  const void* leaf[kChainLeaves];
+  int64_t st[kChainLeaves][4];
+  JFD ext[4];
+  float sc[kChainSteps];
+  float head;
+  void* out;
+  uint32_t n;
+  int pad_;
+};
+
+static const char* kJitPrelude = R"JIT(
+typedef unsigned int uint32_t; typedef long long int64_t; typedef unsigned char uint8_t;
+struct JFD { uint32_t d, m, s; };
+struct JArgs {
+  const void* leaf[8];
+  int64_t st[8][4];
+  JFD ext[4];
+  float sc[16];
+  float head;
+  void* out;
+  uint32_t n;
+  int pad_;
+};
+__device__ __forceinline__ void jdm(const JFD& f, uint32_t n, uint32_t& q, uint32_t& r) {
+  q = (__umulhi(n, f.m) + n) >> f.s; r = n - q * f.d;
+}
+__device__ __forceinline__ float jrcpdiv(float a, float b, float r) {
+  const float aa = fabsf(a), ab = fabsf(b);
+  if (ab >= 0x1p-60f && ab <= 0x1p60f) {
+    if (aa >= 0x1p-60f && aa <= 0x1p60f) {
+      const float q = __fmul_rn(a, r);
+      const float e = __fmaf_rn(-q, b, a);
+      return __fmaf_rn(e, r, q);
+    }
+    if (a == 0.f) return __int_as_float((__float_as_int(a) ^ __float_as_int(b)) & (int)0x80000000);
+  }
+  return a / b;
+}
+__device__ __forceinline__ float jdiv(float a, float b) {
+  const float ab = fabsf(b);
+  if (ab >= 0x1p-60f && ab <= 0x1p60f) return jrcpdiv(a, b, __frcp_rn(b));
+  return a / b;
+}
+__device__ __forceinline__ float jmin(float a, float b) { return ((a != a) || a <= b) ? a : b; }
+__device__ __forceinline__ float jmax(float a, float b) { return ((a != a) || a >= b) ? a : b; }
+)JIT";
+
+typedef int (*NvrtcCreate)(void**, const char*, const char*, int, const char* const*, const char* const*);
+typedef int (*NvrtcCompile)(void*, int, const char* const*);
+typedef int (*NvrtcGetSize)(void*, size_t*);
+typedef int (*NvrtcGet)(void*, char*);
+typedef int (*NvrtcDestroy)(void**);
+typedef CUresult (*CuModuleLoadData)(CUmodule*, const void*);
+typedef CUresult (*CuModuleGetFunction)(CUfunction*, CUmodule, const char*);
+typedef CUresult (*CuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                   CUstream, void**, void**);
+
+struct Jit {
+  bool ok = false;
+  NvrtcCreate create = nullptr;
+  NvrtcCompile compile = nullptr;
+  NvrtcGetSize cubin_size = nullptr, log_size = nullptr;
+  NvrtcGet cubin = nullptr, log = nullptr;
+  NvrtcDestroy destroy = nullptr;
+  CuModuleLoadData load = nullptr;
+  CuModuleGetFunction getfn = nullptr;
+  CuLaunchKernel launch = nullptr;
+  std::mutex mu;
+  std::unordered_map<std::string, CUfunction> cache;
+};
+
+static Jit& jit() {
+  static Jit* j = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    j = new Jit();
+    const char* e = getenv("PB_CHAIN_JIT");
+    if (e && e[0] == '0') return;
+    void* h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    j->create = (NvrtcCreate)dlsym(h, "nvrtcCreateProgram");
+    j->compile = (NvrtcCompile)dlsym(h, "nvrtcCompileProgram");
+    j->cubin_size = (NvrtcGetSize)dlsym(h, "nvrtcGetCUBINSize");
+    j->cubin = (NvrtcGet)dlsym(h, "nvrtcGetCUBIN");
+    j->log_size = (NvrtcGetSize)dlsym(h, "nvrtcGetProgramLogSize");
+    j->log = (NvrtcGet)dlsym(h, "nvrtcGetProgramLog");
+    j->destroy = (NvrtcDestroy)dlsym(h, "nvrtcDestroyProgram");
+    void *f1 = nullptr, *f2 = nullptr, *f3 = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuModuleLoadData", &f1, cudaEnableDefault, &q) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuModuleGetFunction", &f2, cudaEnableDefault, &q) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuLaunchKernel", &f3, cudaEnableDefault, &q) != cudaSuccess)
+      return;
+    j->load = (CuModuleLoadData)f1;
+    j->getfn = (CuModuleGetFunction)f2;
+    j->launch = (CuLaunchKernel)f3;
+    j->ok = j->create && j->compile && j->cubin_size && j->cubin && j->destroy && j->load && j->getfn && j->launch;
+  });
+  return *j;
+}
+
+static const char* jit_bin(int op) {
+  switch (op) {
+    case PB_ADD: return "(a+b)";
+    case PB_SUB: return "(a-b)";
+    case PB_MUL: return "(a*b)";
+    case PB_DIV: return "jdiv(a,b)";
+    case PB_POW: return "powf(a,b)";
+    case PB_MIN: return "jmin(a,b)";
+    case PB_MAX: return "jmax(a,b)";
+    case PB_EQ: return "(a==b?1.f:0.f)";
+    case PB_LT: return "(a<b?1.f:0.f)";
+    case PB_GT: return "(a>b?1.f:0.f)";
+    case PB_AND: return "((a!=0.f&&b!=0.f)?1.f:0.f)";
+    default: return "((a!=0.f||b!=0.f)?1.f:0.f)";
+  }
+}
+static const char* jit_un(int op, int to_bool) {
+  switch (op) {
+    case PB_NEG: return "(-a)";
+    case PB_ABS: return "fabsf(a)";
+    case PB_EXP: return "expf(a)";
+    case PB_LOG: return "logf(a)";
+    case PB_SQRT: return "sqrtf(a)";
+    case PB_SIN: return "sinf(a)";
+    case PB_COS: return "cosf(a)";
+    case PB_TANH: return "tanhf(a)";
+    case PB_NOT: return "(a==0.f?1.f:0.f)";
+    default: return to_bool ? "(a!=0.f?1.f:0.f)" : "a";
+  }
+}
+
+// the kernel source for a chain structure: W = 4 (16-byte leaves along the inner axis) or 1
+static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
+  std::string s = kJitPrelude;
+  s += "extern \"C\" __global__ void __launch_bounds__(256) ew_chain_jit(JArgs p) {\n";
+  s += "  const uint32_t step = gridDim.x * blockDim.x;\n";
+  s += "  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += step) {\n";
+  s += "    uint32_t e = t * " + std::to_string(W) + "u, q, r;\n";
+  for (int l = 0; l < nleaves; ++l) s += "    int64_t o" + std::to_string(l) + " = 0;\n";
+  for (int k = p.nd - 1; k >= 0; --k) {
+    if (k > 0) s += "    jdm(p.ext[" + std::to_string(k) + "], e, q, r);\n";
+    else s += "    q = 0; r = e;\n";
+    for (int l = 0; l < nleaves; ++l) {
+      const std::string L = std::to_string(l);
+      s += "    o" + L + " += (int64_t)r * p.st[" + L + "][" + std::to_string(k) + "];\n";
+    }
+    s += "    e = q;\n";
+  }
+  // leaf loads: x<l>_<lane>
+  for (int l = 0; l < nleaves; ++l) {
+    const std::string L = std::to_string(l);
+    const bool vec = W == 4 && p.vec[l];
+    if (p.is_bool[l]) {
+      if (vec) {
+        s += "    const uchar4 b" + L + " = *reinterpret_cast<const uchar4*>((const uint8_t*)p.leaf[" + L + "] + o" + L + ");\n";
+        const char* c[4] = {"x", "y", "z", "w"};
+        for (int u = 0; u < 4; ++u)
+          s += "    const float x" + L + "_" + std::to_string(u) + " = b" + L + "." + c[u] + " ? 1.f : 0.f;\n";
+      } else {
+        s += "    const float x" + L + "_0 = ((const uint8_t*)p.leaf[" + L + "])[o" + L + "] ? 1.f : 0.f;\n";
+        for (int u = 1; u < W; ++u) s += "    const float x" + L + "_" + std::to_string(u) + " = x" + L + "_0;\n";
+      }
+    } else {
+      if (vec) {
+        s += "    const float4 f" + L + " = __ldg(reinterpret_cast<const float4*>((const float*)p.leaf[" + L + "] + o" + L + "));\n";
+        const char* c[4] = {"x", "y", "z", "w"};
+        for (int u = 0; u < 4; ++u) s += "    const float x" + L + "_" + std::to_string(u) + " = f" + L + "." + c[u] + ";\n";
+      } else {
+        s += "    const float x" + L + "_0 = __ldg((const float*)p.leaf[" + L + "] + o" + L + ");\n";
+        for (int u = 1; u < W; ++u) s += "    const float x" + L + "_" + std::to_string(u) + " = x" + L + "_0;\n";
+      }
+    }
+  }
+  for (int u = 0; u < W; ++u) {
+    const std::string U = std::to_string(u);
+    s += "    float v" + U + " = " + (p.head_kind == 0 ? "x0_" + U : std::string("p.head")) + ";\n";
+  }
+  for (int k = 0; k < p.nsteps; ++k) {
+    const ChainStep& st = p.step[k];
+    for (int u = 0; u < W; ++u) {
+      const std::string U = std::to_string(u);
+      if (st.kind == 0) {
+        s += std::string("    { const float a = v") + U + "; v" + U + " = " + jit_un(st.op - 64, st.to_bool) + "; }\n";
+        continue;
+      }
+      std::string o = st.kind == 1 ? "x" + std::to_string(st.leaf) + "_" + U
+                     : st.kind == 2 ? "p.sc[" + std::to_string(k) + "]" : "v" + U;
+      const std::string a = st.side ? o : "v" + U, b = st.side ? "v" + U : o;
+      s += "    { const float a = " + a + ", b = " + b + "; v" + U + " = " + jit_bin(st.op) + "; }\n";
+    }
+  }
+  if (W == 4) {
+    if (p.out_bool)
+      s += "    reinterpret_cast<uchar4*>(p.out)[t] = make_uchar4(v0 != 0.f, v1 != 0.f, v2 != 0.f, v3 != 0.f);\n";
+    else
+      s += "    reinterpret_cast<float4*>(p.out)[t] = make_float4(v0, v1, v2, v3);\n";
+  } else {
+    s += p.out_bool ? "    ((uint8_t*)p.out)[t] = v0 != 0.f;\n" : "    ((float*)p.out)[t] = v0;\n";
+  }
+  s += "  }\n}\n";
+  return s;
+}
+
+static CUfunction jit_get(const std::string& src) {
+  Jit& j = jit();
+  std::lock_guard<std::mutex> lk(j.mu);
+  auto it = j.cache.find(src);
+  if (it != j.cache.end()) return it->second;
+  CUfunction fn = nullptr;
+  void* prog = nullptr;
+  if (j.create(&prog, src.c_str(), "pb_chain.cu", 0, nullptr, nullptr) == 0) {
+    const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "-std=c++17", "-default-device"};
+    if (j.compile(prog, 4, opts) == 0) {
+      size_t n = 0;
+      if (j.cubin_size(prog, &n) == 0 && n) {
+        std::string bin(n, '\0');
+        CUmodule mod = nullptr;
+        if (j.cubin(prog, &bin[0]) == 0 && j.load(&mod, bin.data()) == CUDA_SUCCESS) j.getfn(&fn, mod, "ew_chain_jit");
+      }
+    }
+    j.destroy(&prog);
+  }
+  j.cache.emplace(src, fn);  // a failure is cached too: that structure stays interpreted
+  return fn;
+}
+
+// launch the JIT kernel for an interpreter-ready ChainArgs; false -> use the interpreter
+static bool jit_chain(const ChainArgs& p, int mode, int nleaves, cudaStream_t s) {
+  if (!jit().ok || nleaves < 1) return false;
+  const int W = (mode == 1 || mode == 3) ? 4 : 1;  // chain4 / chain8 layouts: 16-byte leaves
+  const std::string src = jit_source(p, nleaves, W);
+  CUfunction fn = jit_get(src);
+  if (!fn) return false;
+  JArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int l = 0; l < nleaves; ++l) {
+    a.leaf[l] = p.leaf[l];
+    for (int k = 0; k < 4; ++k) a.st[l][k] = p.st[l][k];
+  }
+  for (int k = 0; k < 4; ++k) a.ext[k] = JFD{p.ext[k].d, p.ext[k].m, p.ext[k].s};
+  for (int k = 0; k < p.nsteps; ++k) a.sc[k] = p.step[k].scalar;
+  a.head = p.head_scalar;
+  a.out = p.out;
+  // the interpreter's element counts: n/4 for chain4, n/8 (in 8s) for chain8, n for chain1 / chain4x
+  uint32_t units = p.n;
+  if (mode == 3) units = p.n * 2;       // chain8 counted 8-element units
+  else if (mode == 2) units = p.n * 4;  // chain4x counted 4-element units of a scalar walk
+  a.n = units;
+  void* args[] = {&a};
+  const unsigned grid = (unsigned)grid_for(units, 256, 2);
+  return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)s, args, nullptr) == CUDA_SUCCESS;
+}
+
 // ----------------------------------------------------------------------- host helpers
 static void fill_dims(Dims& d, const pb_tensor* out, const pb_tensor* a, const pb_tensor* b) {
   d.ndim = out->ndim;
@@ -1941,6 +2215,15 @@ int pb_unary(int op, const pb_tensor* a, int compute, const pb_tensor* out) {
 
 int pb_copy(const pb_tensor* src, const pb_tensor* dst) { return run_cast(src, dst); }
 
+int pb_chain_jit_kernels(void) {
+  Jit& j = jit();
+  if (!j.ok) return -1;
+  std::lock_guard<std::mutex> lk(j.mu);
+  int n = 0;
+  for (auto& kv : j.cache) n += kv.second != nullptr;
+  return n;
+}
+
 int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
                 const pb_chain_step* steps, const pb_tensor* out) {
   int64_t n = numel(*out);
@@ -2057,6 +2340,10 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
   } else {
     for (int l = 0; l < kChainLeaves; ++l) p.vec[l] = 0;
     p.n = (uint32_t)(mode == 2 ? n / 4 : n);
+  }
+  if (jit_chain(p, mode, nleaves, s)) {
+    PB_LAUNCHED();
+    return PB_OK;
   }
   switch (nleaves) {
     case 0: case 1: launch_chain<1>(p, mode, s); break;

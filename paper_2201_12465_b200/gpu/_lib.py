@@ -104,6 +104,7 @@ SIGNATURES = {
     "pb_ew_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _B]),
     "pb_reduce_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _I, _B, _I, _B, _B]),
     "pb_ew_chain_win": (_I, [_I, _B, _B, _I, ctypes.c_double, _I, _B, _B]),
+    "pb_chain_jit_kernels": (_I, []),
     "pb_sgd": (_I, [_I, _U64P, _U64P, _U64P, _U64P, _U64P, _I64P, _F, _F, _F]),
     "pb_bucket_pack": (_I, [_I, _U64P, _I64P, _U64]),
     "pb_scale_f32": (_I, [_U64, ctypes.c_int64, _F]),

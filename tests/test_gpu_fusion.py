@@ -115,3 +115,12 @@ def test_lazy_results_feed_views_and_contractions(pair):
                     h.slice((0, 0), (16, 24), (2, 3)).numpy(), h.sum(axis=1).numpy()])
     for g, w in zip(*res):
         assert np.array_equal(g, w)
+
+
+def test_chain_kernels_are_jit_specialised(pair):
+    """The fused chains above ran as NVRTC-specialised kernels (pb_chain_jit_kernels), not only
+    through the interpreter; their results were already compared bit for bit with the unfused
+    primitives."""
+    from paper_2201_12465_b200.gpu import _lib
+    n = _lib.load().pb_chain_jit_kernels()
+    assert n > 0, n
