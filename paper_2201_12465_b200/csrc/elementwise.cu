@@ -1216,7 +1216,7 @@ static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
   return s;
 }
 
-static CUfunction jit_get(const std::string& src) {
+static CUfunction jit_get(const std::string& src, const char* name = "ew_chain_jit") {
   Jit& j = jit();
   std::lock_guard<std::mutex> lk(j.mu);
   auto it = j.cache.find(src);
@@ -1230,7 +1230,7 @@ static CUfunction jit_get(const std::string& src) {
       if (j.cubin_size(prog, &n) == 0 && n) {
         std::string bin(n, '\0');
         CUmodule mod = nullptr;
-        if (j.cubin(prog, &bin[0]) == 0 && j.load(&mod, bin.data()) == CUDA_SUCCESS) j.getfn(&fn, mod, "ew_chain_jit");
+        if (j.cubin(prog, &bin[0]) == 0 && j.load(&mod, bin.data()) == CUDA_SUCCESS) j.getfn(&fn, mod, name);
       }
     }
     j.destroy(&prog);
@@ -1264,6 +1264,142 @@ static bool jit_chain(const ChainArgs& p, int mode, int nleaves, cudaStream_t s)
   void* args[] = {&a};
   const unsigned grid = (unsigned)grid_for(units, 256, 2);
   return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)s, args, nullptr) == CUDA_SUCCESS;
+}
+
+
+// windowed chains (pb_ew_chain_win) specialised the same way: window parameters stay arguments
+struct JWArgs {
+  const void* leaf[kChainLeaves];
+  int64_t st[kChainLeaves][4];
+  JFD ext[4];
+  int32_t wmul[kChainLeaves][4], woff[kChainLeaves][4], wsh[kChainLeaves][4], wext[kChainLeaves][4];
+  float fill[kChainLeaves];
+  float sc[kChainSteps];
+  float head;
+  void* out;
+  uint32_t n;
+  int pad_;
+};
+static const char* kJitWinDecl = R"JIT(
+struct JWArgs {
+  const void* leaf[8];
+  int64_t st[8][4];
+  JFD ext[4];
+  int wmul[8][4], woff[8][4], wsh[8][4], wext[8][4];
+  float fill[8];
+  float sc[16];
+  float head;
+  void* out;
+  uint32_t n;
+  int pad_;
+};
+)JIT";
+
+static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
+  const ChainArgs& p = a.c;
+  std::string s = kJitPrelude;
+  s += kJitWinDecl;
+  s += "extern \"C\" __global__ void __launch_bounds__(256) ew_chain_win_jit(JWArgs p) {\n";
+  s += "  const uint32_t step = gridDim.x * blockDim.x;\n";
+  s += "  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += step) {\n";
+  s += "    uint32_t q, i0, i1, i2, i3;\n";
+  s += "    jdm(p.ext[3], t * " + std::to_string(W) + "u, q, i3);\n";
+  s += "    jdm(p.ext[2], q, q, i2);\n";
+  s += "    jdm(p.ext[1], q, i0, i1);\n";
+  for (int l = 0; l < nleaves; ++l) {
+    const std::string L = std::to_string(l);
+    const bool isb = p.is_bool[l];
+    auto ldx = [&](const std::string& off) {
+      return isb ? "(((const uint8_t*)p.leaf[" + L + "])[" + off + "] ? 1.f : 0.f)"
+                 : "__ldg((const float*)p.leaf[" + L + "] + " + off + ")";
+    };
+    if (a.w[l].on) {
+      // outer axes once, then each of the W inner positions
+      s += "    int64_t b" + L + " = 0; bool ok" + L + " = true;\n";
+      for (int d = 0; d < 3; ++d) {
+        const std::string D = std::to_string(d);
+        s += "    { const int j = (int)i" + D + " * p.wmul[" + L + "][" + D + "] - p.woff[" + L + "][" + D + "];\n";
+        s += "      const int qq = j >> p.wsh[" + L + "][" + D + "];\n";
+        s += "      ok" + L + " = ok" + L + " && j >= 0 && !(j & ((1 << p.wsh[" + L + "][" + D + "]) - 1)) && qq < p.wext[" + L + "][" + D + "];\n";
+        s += "      b" + L + " += (int64_t)qq * p.st[" + L + "][" + D + "]; }\n";
+      }
+      for (int u = 0; u < W; ++u) {
+        const std::string U = std::to_string(u);
+        s += "    float x" + L + "_" + U + " = p.fill[" + L + "];\n";
+        s += "    { const int j = (int)(i3 + " + U + "u) * p.wmul[" + L + "][3] - p.woff[" + L + "][3];\n";
+        s += "      const int qq = j >> p.wsh[" + L + "][3];\n";
+        s += "      if (ok" + L + " && j >= 0 && !(j & ((1 << p.wsh[" + L + "][3]) - 1)) && qq < p.wext[" + L + "][3])\n";
+        s += "        x" + L + "_" + U + " = " + ldx("b" + L + " + (int64_t)qq * p.st[" + L + "][3]") + "; }\n";
+      }
+    } else {
+      s += "    const int64_t b" + L + " = (int64_t)i0 * p.st[" + L + "][0] + (int64_t)i1 * p.st[" + L + "][1] + (int64_t)i2 * p.st[" + L + "][2];\n";
+      for (int u = 0; u < W; ++u) {
+        const std::string U = std::to_string(u);
+        s += "    const float x" + L + "_" + U + " = " + ldx("b" + L + " + (int64_t)(i3 + " + U + "u) * p.st[" + L + "][3]") + ";\n";
+      }
+    }
+  }
+  for (int u = 0; u < W; ++u) {
+    const std::string U = std::to_string(u);
+    s += "    float v" + U + " = " + (p.head_kind == 0 ? "x0_" + U : std::string("p.head")) + ";\n";
+  }
+  for (int k = 0; k < p.nsteps; ++k) {
+    const ChainStep& st = p.step[k];
+    for (int u = 0; u < W; ++u) {
+      const std::string U = std::to_string(u);
+      if (st.kind == 0) {
+        s += std::string("    { const float a = v") + U + "; v" + U + " = " + jit_un(st.op - 64, st.to_bool) + "; }\n";
+        continue;
+      }
+      std::string o = st.kind == 1 ? "x" + std::to_string(st.leaf) + "_" + U
+                     : st.kind == 2 ? "p.sc[" + std::to_string(k) + "]" : "v" + U;
+      const std::string x = st.side ? o : "v" + U, y = st.side ? "v" + U : o;
+      s += "    { const float a = " + x + ", b = " + y + "; v" + U + " = " + jit_bin(st.op) + "; }\n";
+    }
+  }
+  if (W == 4) {
+    if (p.out_bool)
+      s += "    reinterpret_cast<uchar4*>(p.out)[t] = make_uchar4(v0 != 0.f, v1 != 0.f, v2 != 0.f, v3 != 0.f);\n";
+    else
+      s += "    reinterpret_cast<float4*>(p.out)[t] = make_float4(v0, v1, v2, v3);\n";
+  } else {
+    s += p.out_bool ? "    ((uint8_t*)p.out)[t] = v0 != 0.f;\n" : "    ((float*)p.out)[t] = v0;\n";
+  }
+  s += "  }\n}\n";
+  return s;
+}
+
+static bool jit_win(const WinArgs& a, bool vec, int nleaves, const FastDiv& d1, const FastDiv& d2,
+                    const FastDiv& d3, cudaStream_t st) {
+  if (!jit().ok) return false;
+  const int W = vec ? 4 : 1;
+  const std::string src = jit_win_source(a, nleaves, W);
+  CUfunction fn = jit_get(src, "ew_chain_win_jit");
+  if (!fn) return false;
+  const ChainArgs& p = a.c;
+  JWArgs j;
+  memset(&j, 0, sizeof(j));
+  for (int l = 0; l < nleaves; ++l) {
+    j.leaf[l] = p.leaf[l];
+    j.fill[l] = a.w[l].fill;
+    for (int d = 0; d < 4; ++d) {
+      j.st[l][d] = p.st[l][d];
+      j.wmul[l][d] = a.w[l].mul[d];
+      j.woff[l][d] = a.w[l].off[d];
+      j.wsh[l][d] = a.w[l].shift[d];
+      j.wext[l][d] = a.w[l].ext[d];
+    }
+  }
+  j.ext[1] = JFD{d1.d, d1.m, d1.s};
+  j.ext[2] = JFD{d2.d, d2.m, d2.s};
+  j.ext[3] = JFD{d3.d, d3.m, d3.s};
+  for (int k = 0; k < p.nsteps; ++k) j.sc[k] = p.step[k].scalar;
+  j.head = p.head_scalar;
+  j.out = p.out;
+  j.n = p.n;
+  void* args[] = {&j};
+  const unsigned grid = (unsigned)grid_for(p.n, 256, 2);
+  return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) == CUDA_SUCCESS;
 }
 
 // ----------------------------------------------------------------------- host helpers
@@ -2629,6 +2765,10 @@ int pb_ew_chain_win(int nleaves, const pb_tensor* leaves, const pb_leaf_window* 
   a.d2 = FastDiv((uint32_t)oshape[2]);
   a.d3 = FastDiv((uint32_t)oshape[3]);
   cudaStream_t s = compute_stream();
+  if (jit_win(a, vec, nleaves, a.d1, a.d2, a.d3, s)) {
+    PB_LAUNCHED();
+    return PB_OK;
+  }
   const int grid = grid_for(p.n, 256, 2);
 #define PB_WIN(K)                                              \
   if (vec) ew_chain_win<K><<<grid, 256, 0, s>>>(a);            \
