@@ -973,7 +973,7 @@ class GpuBackend(Backend):
             view = self._times_one(call, args)
             if view is not None:
                 return view
-        if self._fuse and (self._lazy_ok or type(args[0]) in _CHAINABLE or
+        if self._fuse and (self._lazy_ok or self._planned or type(args[0]) in _CHAINABLE or
                            (len(args) > 1 and type(args[1]) in _CHAINABLE)):
             lz = self._try_fuse_binary(call, args)
             if lz is not None:
@@ -1049,7 +1049,7 @@ class GpuBackend(Backend):
             raise DomainError(msg)
 
     def _unary(self, call, args):
-        if self._fuse and (self._lazy_ok or type(args[0]) in _CHAINABLE):
+        if self._fuse and (self._lazy_ok or self._planned or type(args[0]) in _CHAINABLE):
             lz = self._try_fuse_unary(call, args)
             if lz is not None:
                 return lz if self._lazy_ok else lz.dev()
