@@ -1067,6 +1067,7 @@ typedef CUresult (*CuModuleLoadData)(CUmodule*, const void*);
 typedef CUresult (*CuModuleGetFunction)(CUfunction*, CUmodule, const char*);
 typedef CUresult (*CuLaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
                                    CUstream, void**, void**);
+typedef CUresult (*CuOccupancy)(int*, CUfunction, int, size_t);
 
 struct Jit {
   bool ok = false;
@@ -1078,8 +1079,10 @@ struct Jit {
   CuModuleLoadData load = nullptr;
   CuModuleGetFunction getfn = nullptr;
   CuLaunchKernel launch = nullptr;
+  CuOccupancy occupancy = nullptr;
   std::mutex mu;
   std::unordered_map<std::string, CUfunction> cache;
+  std::unordered_map<CUfunction, int> resident;  // 256-thread blocks per SM
 };
 
 static Jit& jit() {
@@ -1108,6 +1111,10 @@ static Jit& jit() {
     j->load = (CuModuleLoadData)f1;
     j->getfn = (CuModuleGetFunction)f2;
     j->launch = (CuLaunchKernel)f3;
+    void* f4 = nullptr;
+    if (cudaGetDriverEntryPoint("cuOccupancyMaxActiveBlocksPerMultiprocessor", &f4, cudaEnableDefault, &q) ==
+        cudaSuccess)
+      j->occupancy = (CuOccupancy)f4;
     j->ok = j->create && j->compile && j->cubin_size && j->cubin && j->destroy && j->load && j->getfn && j->launch;
   });
   return *j;
@@ -1236,7 +1243,25 @@ static CUfunction jit_get(const std::string& src, const char* name = "ew_chain_j
     j.destroy(&prog);
   }
   j.cache.emplace(src, fn);  // a failure is cached too: that structure stays interpreted
+  if (fn) {
+    int b = 0;
+    if (!j.occupancy || j.occupancy(&b, fn, 256, 0) != CUDA_SUCCESS || b < 1) b = 4;
+    j.resident[fn] = b;
+  }
   return fn;
+}
+
+// one full wave of resident blocks, walked grid-stride (no partial second wave)
+static unsigned jit_grid(CUfunction fn, uint32_t units) {
+  int b = 4;
+  {
+    Jit& j = jit();
+    std::lock_guard<std::mutex> lk(j.mu);
+    auto it = j.resident.find(fn);
+    if (it != j.resident.end()) b = it->second;
+  }
+  const uint64_t need = ((uint64_t)units + 255) / 256, wave = (uint64_t)num_sms() * b;
+  return (unsigned)(need < wave ? (need ? need : 1) : wave);
 }
 
 // launch the JIT kernel for an interpreter-ready ChainArgs; false -> use the interpreter
@@ -1262,7 +1287,7 @@ static bool jit_chain(const ChainArgs& p, int mode, int nleaves, cudaStream_t s)
   else if (mode == 2) units = p.n * 4;  // chain4x counted 4-element units of a scalar walk
   a.n = units;
   void* args[] = {&a};
-  const unsigned grid = (unsigned)grid_for(units, 256, 2);
+  const unsigned grid = jit_grid(fn, units);
   return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)s, args, nullptr) == CUDA_SUCCESS;
 }
 
@@ -1398,7 +1423,7 @@ static bool jit_win(const WinArgs& a, bool vec, int nleaves, const FastDiv& d1, 
   j.out = p.out;
   j.n = p.n;
   void* args[] = {&j};
-  const unsigned grid = (unsigned)grid_for(p.n, 256, 2);
+  const unsigned grid = jit_grid(fn, p.n);
   return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) == CUDA_SUCCESS;
 }
 

@@ -1086,11 +1086,13 @@ class GpuBackend(Backend):
         """Run a LazyReduce: one pb_reduce_chain launch for 2-3 stages, else (or when the kernel
         declines the layout) the stages one by one exactly as the eager path runs them."""
         src = lr.src
-        if len(lr.stages) >= 2 and len(src.shape) <= 4:
+        for attempt in range(2):  # a chain the kernel declines is materialised and offered as a plain source
+            if len(lr.stages) < 2 or len(src.shape) > 4:
+                break
             out = self._new(lr.shape, dtypes.f32, "sum")
             if out.block is None:
                 return out
-            if type(src) is LazyArray and src._dev is None:
+            if type(src) is LazyArray and src._dev is None and attempt == 0:
                 leaves, head, steps = src.leaves, src.head, src.steps
             else:
                 leaves, head, steps = (src.dev() if type(src) is LazyArray else src,), ("leaf", 0), ()
@@ -1107,6 +1109,8 @@ class GpuBackend(Backend):
                 return out
             if rc != _lib.UNSUPPORTED:
                 _lib.check(rc, "reduce chain")
+            if type(src) is not LazyArray or src._dev is not None:
+                break
         x = src.dev() if type(src) is LazyArray else src
         for call, _, epi in lr.stages:
             x = self._run_reduce(call, x, epi)
