@@ -472,23 +472,24 @@ __device__ __forceinline__ void split_hl(float x, float& h, float& l) {
 // x[n][c][p] (NCHW, C % 32 == 0) -> hi/lo[n][p][c] (NHWC), a 32x32 tile per block through smem
 __global__ void __launch_bounds__(256) nchw_split_nhwc(const float* __restrict__ x, float* __restrict__ hi,
                                                        float* __restrict__ lo, int C, int P) {
-  // a 32-channel x 64-pixel tile per block: 8 loads in flight per thread before the barrier
-  __shared__ float t[32][65];
-  const int n = blockIdx.z, c0 = blockIdx.y * 32, p0 = blockIdx.x * 64;
+  // a 32-channel x 128-pixel tile per block: 16 loads in flight per thread before the barrier
+  // (a 64-pixel tile left the pass latency-bound at ~2 TB/s: one round trip per 8 KB block)
+  __shared__ float t[32][129];
+  const int n = blockIdx.z, c0 = blockIdx.y * 32, p0 = blockIdx.x * 128;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const float* src = x + ((int64_t)n * C + c0) * P + p0;
-  float v[8];
+  float v[16];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < 16; ++k) {
     const int c = ty + 8 * (k & 3), px = tx + 32 * (k >> 2);
     v[k] = p0 + px < P ? __ldg(src + (int64_t)c * P + px) : 0.f;
   }
 #pragma unroll
-  for (int k = 0; k < 8; ++k) t[ty + 8 * (k & 3)][tx + 32 * (k >> 2)] = v[k];
+  for (int k = 0; k < 16; ++k) t[ty + 8 * (k & 3)][tx + 32 * (k >> 2)] = v[k];
   __syncthreads();
   const int64_t ob = ((int64_t)n * P + p0) * C + c0;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < 16; ++k) {
     const int p = ty + 8 * k;
     if (p0 + p < P) {
       float h, l;
@@ -715,7 +716,7 @@ static int launch(const CUtensorMap& ah, const CUtensorMap& al, const CUtensorMa
 }
 
 static int split_act(const float* x, float* hi, float* lo, int N, int C, int P) {
-  dim3 grid((P + 63) / 64, C / 32, N);
+  dim3 grid((P + 127) / 128, C / 32, N);
   nchw_split_nhwc<<<grid, 256, 0, compute_stream()>>>(x, hi, lo, C, P);
   PB_LAUNCHED();
   return PB_OK;
