@@ -260,6 +260,40 @@ def kernel_roofline(be, T, hbm_peak, tc_peak):
     nbytes = 2 * x.shape.size * 4 + 256 * 4
     out["ew"] = {"bound": "hbm", "achieved": nbytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
                  "kernel": "ew broadcast sub f32 [32,256,56,56]-[1,256,1,1]", "ms": ms}
+    # HBM-bound, the step's largest kernel class by time: a JIT-specialised fused chain -- BatchNorm's
+    # normalise + affine + ReLU over the largest activation, as the planned (captured) step runs it
+    g = T.tensor(rng.standard_normal((1, 256, 1, 1)).astype(np.float32), backend=be.name)
+    bb = T.tensor(rng.standard_normal((1, 256, 1, 1)).astype(np.float32), backend=be.name)
+    sd = T.tensor((rng.random((1, 256, 1, 1)) + 0.5).astype(np.float32), backend=be.name)
+
+    def chain():
+        return ((((x - m) / sd) * g) + bb).maximum(0.0)
+    chain()
+    be.fusion_trace_begin()
+    traced = [chain() for _ in range(10)]
+    be.fusion_trace_end()
+    del traced
+    be.synchronize()
+    be.fusion_plan_begin()
+    try:
+        be.capture_begin()
+        keep = [chain() for _ in range(10)]
+        for k in keep:
+            if hasattr(k.adapter, "materialize"):
+                k.adapter.materialize()
+        graph = be.capture_end()
+    finally:
+        be.fusion_plan_end()
+    graph.launch()
+    be.synchronize()
+    stop = be.event_timer()
+    graph.launch()
+    ms = stop() / 10
+    nbytes = 2 * x.shape.size * 4 + 4 * 256 * 4
+    out["ew_chain_jit"] = {"bound": "hbm", "achieved": nbytes / ms / 1e6, "peak": hbm_peak, "unit": "GB/s",
+                           "frac": nbytes / ms / 1e6 / hbm_peak, "ms": ms,
+                           "kernel": "JIT fused chain max(((x-mean)/std)*gamma+beta, 0) f32 [32,256,56,56], "
+                                     "5 primitives in one launch (device time, graph replay)"}
     return out
 
 

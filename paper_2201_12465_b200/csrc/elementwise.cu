@@ -1157,14 +1157,26 @@ static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
   s += "extern \"C\" __global__ void __launch_bounds__(256) ew_chain_jit(JArgs p) {\n";
   s += "  const uint32_t step = gridDim.x * blockDim.x;\n";
   s += "  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += step) {\n";
+  // 32-bit offsets when every leaf's largest offset fits (strides non-negative)
+  bool small = true;
+  for (int l = 0; l < nleaves && small; ++l) {
+    int64_t mx = 0;
+    for (int k = 0; k < p.nd; ++k) {
+      if (p.st[l][k] < 0) small = false;
+      mx += (int64_t)(p.ext[k].d - 1) * p.st[l][k];
+    }
+    small = small && mx + 4 < ((int64_t)1 << 31);
+  }
+  const char* ot = small ? "uint32_t" : "int64_t";
   s += "    uint32_t e = t * " + std::to_string(W) + "u, q, r;\n";
-  for (int l = 0; l < nleaves; ++l) s += "    int64_t o" + std::to_string(l) + " = 0;\n";
+  for (int l = 0; l < nleaves; ++l) s += std::string("    ") + ot + " o" + std::to_string(l) + " = 0;\n";
   for (int k = p.nd - 1; k >= 0; --k) {
     if (k > 0) s += "    jdm(p.ext[" + std::to_string(k) + "], e, q, r);\n";
     else s += "    q = 0; r = e;\n";
     for (int l = 0; l < nleaves; ++l) {
       const std::string L = std::to_string(l);
-      s += "    o" + L + " += (int64_t)r * p.st[" + L + "][" + std::to_string(k) + "];\n";
+      if (p.st[l][k] == 0) continue;
+      s += "    o" + L + " += (" + ot + ")r * (" + ot + ")p.st[" + L + "][" + std::to_string(k) + "];\n";
     }
     s += "    e = q;\n";
   }
@@ -1199,6 +1211,21 @@ static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
   }
   for (int k = 0; k < p.nsteps; ++k) {
     const ChainStep& st = p.step[k];
+    // a lane-invariant divisor (a scalar or a broadcast leaf): one IEEE reciprocal per thread
+    // iteration, then div_rn_rcp per lane -- the same correctly rounded quotient as jdiv
+    const bool udiv = W > 1 && st.kind != 0 && st.op == PB_DIV && !st.side &&
+                      (st.kind == 2 || (st.kind == 1 && !(W == 4 && p.vec[st.leaf])));
+    if (udiv) {
+      const std::string b = st.kind == 2 ? "p.sc[" + std::to_string(k) + "]" : "x" + std::to_string(st.leaf) + "_0";
+      s += "    { const float bq = " + b + "; const float ab = fabsf(bq);\n";
+      s += "      const bool inr = ab >= 0x1p-60f && ab <= 0x1p60f; const float rq = inr ? __frcp_rn(bq) : 0.f;\n";
+      for (int u = 0; u < W; ++u) {
+        const std::string U = std::to_string(u);
+        s += "      v" + U + " = inr ? jrcpdiv(v" + U + ", bq, rq) : v" + U + " / bq;\n";
+      }
+      s += "    }\n";
+      continue;
+    }
     for (int u = 0; u < W; ++u) {
       const std::string U = std::to_string(u);
       if (st.kind == 0) {
