@@ -745,9 +745,10 @@ static int conv_splits(const Prob& pr) {
   if (tiles >= sms || nkb < 8) return 1;
   int best = 1;
   double best_cost = (double)((tiles + sms - 1) / sms) * nkb;
+  static const double per_kb = getenv("PB_SPLIT_BYTES_PER_KB") ? atof(getenv("PB_SPLIT_BYTES_PER_KB")) : 637500.0;
   for (int sp = 2; sp <= 16 && nkb / sp >= 4; ++sp) {
     const double cost = (double)((tiles * sp + sms - 1) / sms) * ((nkb + sp - 1) / sp) +
-                        (double)pr.Mi * pr.Nj * sp / 637500.0;  // ~one k-block per 2.5 MB of partials
+                        (double)pr.Mi * pr.Nj * sp / per_kb;  // ~one k-block per 2.5 MB of partials
     if (cost < best_cost * 0.95) {
       best = sp;
       best_cost = cost;
