@@ -1347,7 +1347,11 @@ struct JWArgs {
 };
 )JIT";
 
-static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
+// ragged (W = 4 over rows whose length is not a multiple of 4 -- the maxpool backward's 114-wide
+// padded planes): a thread takes 4 consecutive positions of one row, so the outer-axis window
+// checks run once per 4 outputs instead of per output; positions past the row end are masked
+// (ext[0] = 4-groups per row, pad_ = the row length)
+static std::string jit_win_source(const WinArgs& a, int nleaves, int W, bool ragged) {
   const ChainArgs& p = a.c;
   std::string s = kJitPrelude;
   s += kJitWinDecl;
@@ -1355,7 +1359,15 @@ static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
   s += "  const uint32_t step = gridDim.x * blockDim.x;\n";
   s += "  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < p.n; t += step) {\n";
   s += "    uint32_t q, i0, i1, i2, i3;\n";
-  s += "    jdm(p.ext[3], t * " + std::to_string(W) + "u, q, i3);\n";
+  if (ragged) {
+    s += "    uint32_t row, g;\n";
+    s += "    const uint32_t inner = (uint32_t)p.pad_;\n";
+    s += "    jdm(p.ext[0], t, row, g);\n";
+    s += "    i3 = g * 4u;\n";
+    s += "    q = row;\n";
+  } else {
+    s += "    jdm(p.ext[3], t * " + std::to_string(W) + "u, q, i3);\n";
+  }
   s += "    jdm(p.ext[2], q, q, i2);\n";
   s += "    jdm(p.ext[1], q, i0, i1);\n";
   for (int l = 0; l < nleaves; ++l) {
@@ -1380,14 +1392,16 @@ static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
         s += "    float x" + L + "_" + U + " = p.fill[" + L + "];\n";
         s += "    { const int j = (int)(i3 + " + U + "u) * p.wmul[" + L + "][3] - p.woff[" + L + "][3];\n";
         s += "      const int qq = j >> p.wsh[" + L + "][3];\n";
-        s += "      if (ok" + L + " && j >= 0 && !(j & ((1 << p.wsh[" + L + "][3]) - 1)) && qq < p.wext[" + L + "][3])\n";
+        s += "      if (ok" + L + " && j >= 0 && !(j & ((1 << p.wsh[" + L + "][3]) - 1)) && qq < p.wext[" + L + "][3]" +
+             (ragged ? " && i3 + " + U + "u < inner" : "") + ")\n";
         s += "        x" + L + "_" + U + " = " + ldx("b" + L + " + (int64_t)qq * p.st[" + L + "][3]") + "; }\n";
       }
     } else {
       s += "    const int64_t b" + L + " = (int64_t)i0 * p.st[" + L + "][0] + (int64_t)i1 * p.st[" + L + "][1] + (int64_t)i2 * p.st[" + L + "][2];\n";
       for (int u = 0; u < W; ++u) {
         const std::string U = std::to_string(u);
-        s += "    const float x" + L + "_" + U + " = " + ldx("b" + L + " + (int64_t)(i3 + " + U + "u) * p.st[" + L + "][3]") + ";\n";
+        const std::string ld = ldx("b" + L + " + (int64_t)(i3 + " + U + "u) * p.st[" + L + "][3]");
+        s += "    const float x" + L + "_" + U + " = " + (ragged ? "i3 + " + U + "u < inner ? " + ld + " : 0.f" : ld) + ";\n";
       }
     }
   }
@@ -1409,7 +1423,15 @@ static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
       s += "    { const float a = " + x + ", b = " + y + "; v" + U + " = " + jit_bin(st.op) + "; }\n";
     }
   }
-  if (W == 4) {
+  if (ragged) {
+    s += "    const int64_t ob = (int64_t)row * inner + i3;\n";
+    for (int u = 0; u < 4; ++u) {
+      const std::string U = std::to_string(u);
+      s += "    if (i3 + " + U + "u < inner) " +
+           (p.out_bool ? "((uint8_t*)p.out)[ob + " + U + "] = v" + U + " != 0.f;\n"
+                       : "((float*)p.out)[ob + " + U + "] = v" + U + ";\n");
+    }
+  } else if (W == 4) {
     if (p.out_bool)
       s += "    reinterpret_cast<uchar4*>(p.out)[t] = make_uchar4(v0 != 0.f, v1 != 0.f, v2 != 0.f, v3 != 0.f);\n";
     else
@@ -1422,10 +1444,11 @@ static std::string jit_win_source(const WinArgs& a, int nleaves, int W) {
 }
 
 static bool jit_win(const WinArgs& a, bool vec, int nleaves, const FastDiv& d1, const FastDiv& d2,
-                    const FastDiv& d3, cudaStream_t st) {
+                    const FastDiv& d3, cudaStream_t st, uint32_t inner = 0) {
   if (!jit().ok) return false;
-  const int W = vec ? 4 : 1;
-  const std::string src = jit_win_source(a, nleaves, W);
+  const bool ragged = !vec && inner >= 8;
+  const int W = vec || ragged ? 4 : 1;
+  const std::string src = jit_win_source(a, nleaves, W, ragged);
   CUfunction fn = jit_get(src, "ew_chain_win_jit");
   if (!fn) return false;
   const ChainArgs& p = a.c;
@@ -1449,8 +1472,15 @@ static bool jit_win(const WinArgs& a, bool vec, int nleaves, const FastDiv& d1, 
   j.head = p.head_scalar;
   j.out = p.out;
   j.n = p.n;
+  if (ragged) {
+    const uint32_t groups = (inner + 3) / 4;
+    const FastDiv gd(groups);
+    j.ext[0] = JFD{gd.d, gd.m, gd.s};
+    j.pad_ = (int)inner;
+    j.n = p.n / inner * groups;  // (p.n = every output element here)
+  }
   void* args[] = {&j};
-  const unsigned grid = jit_grid(fn, p.n);
+  const unsigned grid = jit_grid(fn, j.n);
   return jit().launch(fn, grid, 1, 1, 256, 1, 1, 0, (CUstream)st, args, nullptr) == CUDA_SUCCESS;
 }
 
@@ -2817,7 +2847,7 @@ int pb_ew_chain_win(int nleaves, const pb_tensor* leaves, const pb_leaf_window* 
   a.d2 = FastDiv((uint32_t)oshape[2]);
   a.d3 = FastDiv((uint32_t)oshape[3]);
   cudaStream_t s = compute_stream();
-  if (jit_win(a, vec, nleaves, a.d1, a.d2, a.d3, s)) {
+  if (jit_win(a, vec, nleaves, a.d1, a.d2, a.d3, s, (uint32_t)oshape[3])) {
     PB_LAUNCHED();
     return PB_OK;
   }
