@@ -156,6 +156,13 @@ typedef struct pb_chain_step {
 } pb_chain_step;
 int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
                 const pb_chain_step* steps, const pb_tensor* out);
+/* The chain above that also stores its running value after tap_after[i] steps (1..nsteps) into
+ * taps[i] (dense, 16-byte aligned f32 of out's size): a multi-use intermediate of the chain is
+ * written by the pass that consumes it instead of by a pass of its own (round 2 "taps").  JIT
+ * kernels only: PB_ERR_UNSUPPORTED, with nothing launched, when the chain cannot be specialised. */
+int pb_ew_chain_taps(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                     const pb_chain_step* steps, int ntaps, const int* tap_after, const pb_tensor* taps,
+                     const pb_tensor* out);
 /* Chain kernels specialised per structure with NVRTC (straight-line code, the same functors and
  * flags as the interpreter: bit-identical); this returns how many are compiled and cached, or -1
  * when the JIT is off (PB_CHAIN_JIT=0 or libnvrtc missing: the interpreter runs every chain). */

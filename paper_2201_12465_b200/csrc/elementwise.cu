@@ -454,6 +454,7 @@ __global__ void fastdiv_probe(const float* a, const float* b, float* out, int64_
 // fused chain is bit-identical to running its primitives one by one.
 static const int kChainLeaves = 8;
 static const int kChainSteps = 16;
+static const int kChainTaps = 4;
 
 struct ChainStep {
   int16_t op;    // pb_binop, or 64 + pb_unop (PB_CAST: to the step's bool flag)
@@ -478,6 +479,10 @@ struct ChainArgs {
   FastDiv ext[4];
   int64_t st[kChainLeaves][4];
   uint32_t n;
+  // taps (JIT only): after tap_after[i] steps, v is also stored to tap[i] (dense f32, out's shape)
+  int ntaps;
+  int8_t tap_after[kChainTaps];
+  void* tap[kChainTaps];
 };
 
 template <int NL>
@@ -1019,6 +1024,7 @@ struct JArgs {
   void* out;
   uint32_t n;
   int pad_;
+  void* tap[kChainTaps];
 };
 
 static const char* kJitPrelude = R"JIT(
@@ -1033,6 +1039,7 @@ struct JArgs {
   void* out;
   uint32_t n;
   int pad_;
+  void* tap[4];
 };
 __device__ __forceinline__ void jdm(const JFD& f, uint32_t n, uint32_t& q, uint32_t& r) {
   q = (__umulhi(n, f.m) + n) >> f.s; r = n - q * f.d;
@@ -1151,6 +1158,16 @@ static const char* jit_un(int op, int to_bool) {
   }
 }
 
+// tap stores after `after` steps: output element t*W + u of each tap is this lane's v
+static void jit_taps(std::string& s, const ChainArgs& p, int after, int W) {
+  for (int i = 0; i < p.ntaps; ++i) {
+    if (p.tap_after[i] != after) continue;
+    const std::string I = std::to_string(i);
+    if (W == 4) s += "    reinterpret_cast<float4*>(p.tap[" + I + "])[t] = make_float4(v0, v1, v2, v3);\n";
+    else s += "    ((float*)p.tap[" + I + "])[t] = v0;\n";
+  }
+}
+
 // the kernel source for a chain structure: W = 4 (16-byte leaves along the inner axis) or 1
 static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
   std::string s = kJitPrelude;
@@ -1224,6 +1241,7 @@ static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
         s += "      v" + U + " = inr ? jrcpdiv(v" + U + ", bq, rq) : v" + U + " / bq;\n";
       }
       s += "    }\n";
+      jit_taps(s, p, k + 1, W);
       continue;
     }
     for (int u = 0; u < W; ++u) {
@@ -1237,6 +1255,7 @@ static std::string jit_source(const ChainArgs& p, int nleaves, int W) {
       const std::string a = st.side ? o : "v" + U, b = st.side ? "v" + U : o;
       s += "    { const float a = " + a + ", b = " + b + "; v" + U + " = " + jit_bin(st.op) + "; }\n";
     }
+    jit_taps(s, p, k + 1, W);
   }
   if (W == 4) {
     if (p.out_bool)
@@ -1308,6 +1327,7 @@ static bool jit_chain(const ChainArgs& p, int mode, int nleaves, cudaStream_t s)
   for (int k = 0; k < p.nsteps; ++k) a.sc[k] = p.step[k].scalar;
   a.head = p.head_scalar;
   a.out = p.out;
+  for (int i = 0; i < p.ntaps; ++i) a.tap[i] = p.tap[i];
   // the interpreter's element counts: n/4 for chain4, n/8 (in 8s) for chain8, n for chain1 / chain4x
   uint32_t units = p.n;
   if (mode == 3) units = p.n * 2;       // chain8 counted 8-element units
@@ -2128,10 +2148,45 @@ __device__ __forceinline__ void rc_load_batch(const RCArgs& p, const int64_t (&o
   }
 }
 
-template <int NL, int B, bool V4, bool PLAIN>
+// product source (round 2): v = x0 * x0 (BatchNorm's c * c) or x0 * x1 (the gamma gradient's
+// g * xhat), f32 leaves -- the interpreter's one MUL step without its dispatch and registers
+template <int NL, int B, bool V4>
+__device__ __forceinline__ void rc_mul_batch(const RCArgs& p, const int64_t (&off)[B][NL], const bool (&on)[B],
+                                             float4 (&v)[B]) {
+  float4 y[B];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const float* f = (const float*)p.leaf[l];
+    const bool vec = V4 && p.s_vec[l];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on[u]) {
+        if (vec) {
+          t = __ldg(reinterpret_cast<const float4*>(f + off[u][l]));
+        } else {
+          const float q = __ldg(f + off[u][l]);
+          t = make_float4(q, q, q, q);
+        }
+      }
+      if (l == 0) v[u] = t;
+      else y[u] = t;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    const float4 w = NL > 1 ? y[u] : v[u];
+    v[u] = make_float4(Bin<PB_MUL, float>::f(v[u].x, w.x), Bin<PB_MUL, float>::f(v[u].y, w.y),
+                       Bin<PB_MUL, float>::f(v[u].z, w.z), Bin<PB_MUL, float>::f(v[u].w, w.w));
+  }
+}
+
+// SRC 1: plain source; 2: product source; 0: the interpreter
+template <int NL, int B, bool V4, int SRC>
 __device__ __forceinline__ void rc_source(const RCArgs& p, const int64_t (&off)[B][NL], const bool (&on)[B],
                                           float4 (&v)[B]) {
-  if constexpr (PLAIN) rc_load_batch<B, V4>(p, off, on, v);
+  if constexpr (SRC == 1) rc_load_batch<B, V4>(p, off, on, v);
+  else if constexpr (SRC == 2) rc_mul_batch<NL, B, V4>(p, off, on, v);
   else rc_eval_batch<NL, B, V4>(p, off, on, v);
 }
 
@@ -2161,7 +2216,7 @@ __device__ __forceinline__ void rc_group_base(const RCArgs& p, int g, int64_t (&
 // rows allow -- then a thread per row sums it in f64 (4 chains) from the odd-pitch (conflict-free)
 // buffer, a warp per plane folds the rows (stage 2), and stage 3 folds the planes: in the block when
 // it holds them all, else through the workspace in the group's last block (ticket)
-template <int NL, bool V4, bool PLAIN>
+template <int NL, bool V4, int SRC>
 __global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
   extern __shared__ float rc_smem[];
   constexpr int VW = V4 ? 4 : 1;
@@ -2172,7 +2227,7 @@ __global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
   const int i3a = sp * p.r3, np = min(p.r3, p.E3 - i3a);
   int64_t gb[NL];
   rc_group_base<NL>(p, g, gb);
-  constexpr int B = PLAIN ? 8 : (NL <= 3 ? 4 : 2);
+  constexpr int B = SRC == 1 ? 8 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
   const int units = np * p.E2 * p.U1;
   for (int u0 = threadIdx.x; u0 < units; u0 += B * blockDim.x) {
     float4 v[B];
@@ -2191,7 +2246,7 @@ __global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
       for (int l = 0; l < NL; ++l) off[k][l] = gb[l] + i3 * p.s3[l] + (int64_t)i2 * p.s2[l] + i1 * p.s1[l];
       dst[k] = (int)(pi * p.E2 + i2) * p.E1p + (int)i1;
     }
-    rc_source<NL, B, V4, PLAIN>(p, off, on, v);
+    rc_source<NL, B, V4, SRC>(p, off, on, v);
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       if (on[k]) {
@@ -2263,7 +2318,7 @@ __global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
 // in order through shared memory.  Stage 2 sums the block's rows per column in f64; with several
 // blocks per group those f64 partials meet in the group's last block (ticket), which rounds them,
 // applies the stage-2 epilogue and folds stage 3.
-template <int NL, bool V4, bool PLAIN>
+template <int NL, bool V4, int SRC>
 __global__ void __launch_bounds__(256) redchain_cols(RCArgs p) {
   extern __shared__ float rc_smem[];
   constexpr int VW = V4 ? 4 : 1;
@@ -2289,7 +2344,7 @@ __global__ void __launch_bounds__(256) redchain_cols(RCArgs p) {
       int64_t po[NL];
 #pragma unroll
       for (int l = 0; l < NL; ++l) po[l] = gb[l] + (int64_t)i3 * p.s3[l] + (int64_t)(h0 + hl) * p.s2[l];
-      constexpr int B = PLAIN ? 16 : (NL <= 3 ? 4 : 2);
+      constexpr int B = SRC == 1 ? 16 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
       for (int j = j0; j < j1; j += B) {
         float4 v[B];
         int64_t off[B][NL];
@@ -2300,7 +2355,7 @@ __global__ void __launch_bounds__(256) redchain_cols(RCArgs p) {
 #pragma unroll
           for (int l = 0; l < NL; ++l) off[u][l] = po[l] + (int64_t)(j + u) * p.s1[l];
         }
-        rc_source<NL, B, V4, PLAIN>(p, off, on, v);
+        rc_source<NL, B, V4, SRC>(p, off, on, v);
 #pragma unroll
         for (int u = 0; u < B; ++u) {
           if (on[u]) {
@@ -2382,22 +2437,22 @@ static void rc_smem_attr(K k) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024);
 }
 
-template <int NL, bool PLAIN>
+template <int NL, int SRC>
 static void launch_redchain(const RCArgs& p, bool rows, bool v4, int grid, int threads, size_t smem, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    rc_smem_attr(redchain_rows<NL, true, PLAIN>);
-    rc_smem_attr(redchain_rows<NL, false, PLAIN>);
-    rc_smem_attr(redchain_cols<NL, true, PLAIN>);
-    rc_smem_attr(redchain_cols<NL, false, PLAIN>);
+    rc_smem_attr(redchain_rows<NL, true, SRC>);
+    rc_smem_attr(redchain_rows<NL, false, SRC>);
+    rc_smem_attr(redchain_cols<NL, true, SRC>);
+    rc_smem_attr(redchain_cols<NL, false, SRC>);
     attr = true;
   }
   if (rows) {
-    if (v4) redchain_rows<NL, true, PLAIN><<<grid, threads, smem, s>>>(p);
-    else redchain_rows<NL, false, PLAIN><<<grid, threads, smem, s>>>(p);
+    if (v4) redchain_rows<NL, true, SRC><<<grid, threads, smem, s>>>(p);
+    else redchain_rows<NL, false, SRC><<<grid, threads, smem, s>>>(p);
   } else {
-    if (v4) redchain_cols<NL, true, PLAIN><<<grid, threads, smem, s>>>(p);
-    else redchain_cols<NL, false, PLAIN><<<grid, threads, smem, s>>>(p);
+    if (v4) redchain_cols<NL, true, SRC><<<grid, threads, smem, s>>>(p);
+    else redchain_cols<NL, false, SRC><<<grid, threads, smem, s>>>(p);
   }
 }
 
@@ -2442,8 +2497,30 @@ int pb_chain_jit_kernels(void) {
   return n;
 }
 
+static int ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                    const pb_chain_step* steps, int ntaps, const int* tap_after, const pb_tensor* taps,
+                    const pb_tensor* out);
+
 int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
                 const pb_chain_step* steps, const pb_tensor* out) {
+  return ew_chain(nleaves, leaves, head_kind, head_scalar, nsteps, steps, 0, nullptr, nullptr, out);
+}
+
+int pb_ew_chain_taps(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                     const pb_chain_step* steps, int ntaps, const int* tap_after, const pb_tensor* taps,
+                     const pb_tensor* out) {
+  if (ntaps < 0 || ntaps > kChainTaps) return fail(PB_ERR_ARG, "pb_ew_chain_taps: 0..4 taps");
+  for (int i = 0; i < ntaps; ++i) {
+    if (tap_after[i] < 1 || tap_after[i] > nsteps) return fail(PB_ERR_ARG, "pb_ew_chain_taps: tap step out of range");
+    if (taps[i].dtype != PB_F32 || !is_contiguous(taps[i]) || numel(taps[i]) != numel(*out) || (taps[i].ptr & 15))
+      return fail(PB_ERR_ARG, "pb_ew_chain_taps: a tap is a dense, 16-byte aligned f32 tensor of the output's size");
+  }
+  return ew_chain(nleaves, leaves, head_kind, head_scalar, nsteps, steps, ntaps, tap_after, taps, out);
+}
+
+static int ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head_scalar, int nsteps,
+                    const pb_chain_step* steps, int ntaps, const int* tap_after, const pb_tensor* taps,
+                    const pb_tensor* out) {
   int64_t n = numel(*out);
   if (n == 0) return PB_OK;
   if (nleaves < 0 || nleaves > kChainLeaves || nsteps < 0 || nsteps > kChainSteps ||
@@ -2559,10 +2636,16 @@ int pb_ew_chain(int nleaves, const pb_tensor* leaves, int head_kind, double head
     for (int l = 0; l < kChainLeaves; ++l) p.vec[l] = 0;
     p.n = (uint32_t)(mode == 2 ? n / 4 : n);
   }
+  p.ntaps = ntaps;
+  for (int i = 0; i < ntaps; ++i) {
+    p.tap_after[i] = (int8_t)tap_after[i];
+    p.tap[i] = (void*)(uintptr_t)taps[i].ptr;
+  }
   if (jit_chain(p, mode, nleaves, s)) {
     PB_LAUNCHED();
     return PB_OK;
   }
+  if (ntaps) return fail(PB_ERR_UNSUPPORTED, "pb_ew_chain_taps: taps need the JIT chain kernels");
   switch (nleaves) {
     case 0: case 1: launch_chain<1>(p, mode, s); break;
     case 2: launch_chain<2>(p, mode, s); break;
@@ -2764,13 +2847,20 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
   if (grid >= ((int64_t)1 << 31)) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: grid");
   cudaStream_t s = compute_stream();
   const bool plain = nleaves == 1 && nsteps == 0 && head_kind == 0 && !p.is_bool[0];
-  switch (plain ? 0 : nleaves) {
-    case 0: launch_redchain<1, true>(p, rows, v4, (int)grid, threads, smem, s); break;
-    case 1: launch_redchain<1, false>(p, rows, v4, (int)grid, threads, smem, s); break;
-    case 2: launch_redchain<2, false>(p, rows, v4, (int)grid, threads, smem, s); break;
-    case 3: launch_redchain<3, false>(p, rows, v4, (int)grid, threads, smem, s); break;
-    case 4: launch_redchain<4, false>(p, rows, v4, (int)grid, threads, smem, s); break;
-    default: launch_redchain<8, false>(p, rows, v4, (int)grid, threads, smem, s); break;
+  // product: one MUL of leaf 0 by itself (x0 * x0) or by leaf 1 (either side: IEEE a*b == b*a)
+  static const bool interp_only = getenv("PB_RC_INTERP") != nullptr;  // experiment hook
+  const bool product = !interp_only && nsteps == 1 && head_kind == 0 && steps[0].op == PB_MUL &&
+                       ((nleaves == 1 && steps[0].kind == 3) || (nleaves == 2 && steps[0].kind == 1 && steps[0].leaf == 1)) &&
+                       !p.is_bool[0] && (nleaves == 1 || !p.is_bool[1]);
+  switch (plain ? 0 : product ? -nleaves : nleaves) {
+    case 0: launch_redchain<1, 1>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case -1: launch_redchain<1, 2>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case -2: launch_redchain<2, 2>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 1: launch_redchain<1, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 2: launch_redchain<2, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 3: launch_redchain<3, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case 4: launch_redchain<4, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
+    default: launch_redchain<8, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
   }
   PB_LAUNCHED();
   return PB_OK;

@@ -102,6 +102,7 @@ SIGNATURES = {
     "pb_conv2d_grad_input": (_I, [_B, _B, _B, _B]),
     "pb_conv2d_grad_weight": (_I, [_B, _B, _B, _B]),
     "pb_ew_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _B]),
+    "pb_ew_chain_taps": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _I, _B, _B, _B]),
     "pb_reduce_chain": (_I, [_I, _B, _I, ctypes.c_double, _I, _B, _I, _B, _I, _B, _B]),
     "pb_ew_chain_win": (_I, [_I, _B, _B, _I, ctypes.c_double, _I, _B, _B]),
     "pb_chain_jit_kernels": (_I, []),

@@ -115,9 +115,9 @@ class LazyArray:
     """
 
     __slots__ = ("be", "shape", "strides", "dtype", "host", "leaves", "head", "steps", "uses", "_dev",
-                 "__weakref__")
+                 "taps", "tap_ok", "__weakref__")
 
-    def __init__(self, be, shape, dtype, leaves, head, steps):
+    def __init__(self, be, shape, dtype, leaves, head, steps, taps=()):
         self.be = be
         self.shape = shape
         self.strides = contig_strides(shape)
@@ -128,12 +128,18 @@ class LazyArray:
         self.steps = steps    # tuple of (op, kind, side, leaf, to_bool, scalar)
         self.uses = 0
         self._dev = None
+        # taps: ((steps applied, LazyArray), ...) -- multi-use intermediates of this chain that
+        # its kernel also stores (pb_ew_chain_taps); tap_ok: this result is such an
+        # intermediate (the plan saw several consumers, the first one elementwise)
+        self.taps = taps
+        self.tap_ok = False
 
     def dev(self):
         d = self._dev
         if d is None:
             d = self._dev = self.be._run_chain(self)
             self.leaves = self.steps = None
+            self.taps = ()
         return d
 
     def materialize(self):
@@ -160,6 +166,8 @@ _FUSE_BIN = {"add", "sub", "mul", "div", "pow", "minimum", "maximum", "eq", "lt"
 _FUSE_UN = {"neg", "abs", "exp", "log", "sqrt", "sin", "cos", "tanh", "logical_not", "astype"}
 _MAX_LEAVES, _MAX_STEPS = 8, 16
 _MAX_USES = int(os.environ.get("PB_FUSE_USES", "1"))  # consumers that may recompute one chain
+_MAX_TAPS = 4
+_TAPS = os.environ.get("PB_FUSE_TAPS", "1") != "0"  # experiment hook: 0 materialises multi-use chains alone
 
 
 _LOGICAL = ("logical_and", "logical_or")
@@ -385,6 +393,7 @@ class GpuBackend(Backend):
         self._lazy_ok = True
         self._lazy_red = False
         self._lazy_epi = False
+        self._lazy_tap = False
         self._lib = _lib.load()
         _lib.check(self._lib.pb_init(device), "pb_init")
         self.device = device
@@ -524,11 +533,12 @@ class GpuBackend(Backend):
             red_ax = name == "sum" and call.dtype is dtypes.f32 and call.params.get("axis") is not None
             self._trace.append((sig, prods, fusible, epi, red_ax))
         else:
-            tr, lazy, lazy_red, lazy_epi = self._plan
+            tr, lazy, lazy_red, lazy_epi, tap = self._plan
             if idx < len(tr) and tr[idx][0] == sig and tr[idx][1] == prods:
                 self._lazy_ok = lazy[idx]
                 self._lazy_red = lazy_red[idx]
                 self._lazy_epi = lazy_epi[idx]
+                self._lazy_tap = tap[idx]
             else:  # the step diverged from the trace: stop fusing (everything materialises)
                 self._abandon_plan()
         res = self._execute(call, args)
@@ -583,8 +593,27 @@ class GpuBackend(Backend):
             return is_sum[d] or (lazy_epi[d] and is_sum[cons[d]])
 
         lazy = [tr[i][2] and one[i] and (by_fusible[i] or opens_chain(cons[i])) for i in range(n)]
-        self._plan = (tr, lazy, lazy_red, lazy_epi)
-        return sum(lazy) + sum(lazy_red) + sum(lazy_epi)
+        # taps: an f32 elementwise result with several consumers, the first of them an
+        # elementwise op of the same shape, stays pending; that consumer's chain kernel stores it
+        first = [-1] * n
+        for j in range(n - 1, -1, -1):
+            for q in tr[j][1]:
+                if q >= 0:
+                    first[q] = j
+        def chain_end(j):  # where the consumer's chain is run: past its planned-lazy links
+            while lazy[j] and cons[j] >= 0:
+                j = cons[j]
+            return j
+
+        def runs_as_chain(j):  # a materialised elementwise result (not a reduction's source)
+            return tr[j][2] and tr[j][0][0] != "slice"
+
+        tap = [_TAPS and tr[i][2] and not lazy[i] and uses[i] >= 2 and tr[i][0][2] == "f32" and
+               tr[i][0][0] != "slice" and first[i] >= 0 and runs_as_chain(first[i]) and
+               tr[first[i]][0][1] == tr[i][0][1] and runs_as_chain(chain_end(first[i])) and
+               tr[chain_end(first[i])][0][1] == tr[i][0][1] for i in range(n)]
+        self._plan = (tr, lazy, lazy_red, lazy_epi, tap)
+        return sum(lazy) + sum(lazy_red) + sum(lazy_epi) + sum(tap)
 
     def fusion_plan_begin(self):
         """Replay the planned step (normally while recording a CUDA graph): ops the plan marks
@@ -599,7 +628,8 @@ class GpuBackend(Backend):
         self._lazy_ok = False
         self._lazy_red = False
         self._lazy_epi = False
-        self._plan = ([], [], [], [])
+        self._lazy_tap = False
+        self._plan = ([], [], [], [], [])
 
     @property
     def plan_abandoned(self):
@@ -613,6 +643,7 @@ class GpuBackend(Backend):
         self._lazy_ok = True
         self._lazy_red = False
         self._lazy_epi = False
+        self._lazy_tap = False
 
     def synchronize(self):
         _lib.check(self._lib.pb_synchronize(), "synchronize")
@@ -839,16 +870,26 @@ class GpuBackend(Backend):
         """A DeviceArray for a chain leaf (lazy operands that are not extended run now)."""
         return a.dev() if type(a) is LazyArray else a
 
-    def _extendable(self, a, extra_steps=1, extra_leaves=1):
-        return (type(a) is LazyArray and a._dev is None and a.uses < _MAX_USES
-                and len(a.steps) + extra_steps <= _MAX_STEPS and len(a.leaves) + extra_leaves <= _MAX_LEAVES)
+    def _extendable(self, a, extra_steps=1, extra_leaves=1, shape=None):
+        if not (type(a) is LazyArray and a._dev is None and a.uses < _MAX_USES
+                and len(a.steps) + extra_steps <= _MAX_STEPS and len(a.leaves) + extra_leaves <= _MAX_LEAVES):
+            return False
+        if a.tap_ok or a.taps:  # taps are stored at the chain's output index: same shape only
+            if shape is None or tuple(shape) != a.shape or len(a.taps) + a.tap_ok > _MAX_TAPS:
+                return False
+            if any(type(d) is LazyWindow for d in a.leaves):
+                return False
+        return True
 
-    def _chain_from(self, a):
-        """(leaves list, head, steps list) to extend: a's chain, or a fresh one rooted at leaf a."""
-        if type(a) is LazyArray and self._extendable(a):
+    def _chain_from(self, a, shape=None):
+        """(leaves list, head, steps list, taps) to extend: a's chain, or a fresh one rooted at
+        leaf a.  Extending a multi-use intermediate (tap_ok) taps it: the extended chain's kernel
+        stores a's value after a's steps."""
+        if type(a) is LazyArray and self._extendable(a, shape=shape):
             a.uses += 1
-            return list(a.leaves), a.head, list(a.steps)
-        return [self._as_leaf(a)], ("leaf", 0), []
+            taps = a.taps + (((len(a.steps), a),) if a.tap_ok else ())
+            return list(a.leaves), a.head, list(a.steps), taps
+        return [self._as_leaf(a)], ("leaf", 0), [], ()
 
     @staticmethod
     def _leaf_index(leaves, d):
@@ -885,7 +926,7 @@ class GpuBackend(Backend):
                 pass  # representable as f32 either way
             elif abs(fv) > 3.4e38:
                 return None
-            leaves, head, steps = self._chain_from(a)
+            leaves, head, steps, taps = self._chain_from(a, call.shape)
             side = 1 if p.get("scalar_side") == "left" else 0
             steps.append((code, 2, side, 0, 0, fv))
         else:
@@ -896,19 +937,19 @@ class GpuBackend(Backend):
             if ct is not dtypes.f32 and not (ct is dtypes.bool_ and name in _LOGICAL):
                 return None
             if a is b:
-                leaves, head, steps = self._chain_from(a)
+                leaves, head, steps, taps = self._chain_from(a, call.shape)
                 steps.append((code, 3, 0, 0, 0, 0.0))
-            elif self._extendable(a) or not self._extendable(b):
-                leaves, head, steps = self._chain_from(a)
+            elif self._extendable(a, shape=call.shape) or not self._extendable(b, shape=call.shape):
+                leaves, head, steps, taps = self._chain_from(a, call.shape)
                 if len(leaves) >= _MAX_LEAVES:
                     return None
                 steps.append((code, 1, 0, self._leaf_index(leaves, self._as_leaf(b)), 0, 0.0))
             else:
-                leaves, head, steps = self._chain_from(b)
+                leaves, head, steps, taps = self._chain_from(b, call.shape)
                 if len(leaves) >= _MAX_LEAVES:
                     return None
                 steps.append((code, 1, 1, self._leaf_index(leaves, self._as_leaf(a)), 0, 0.0))
-        return LazyArray(self, tuple(call.shape), out_dt, tuple(leaves), head, tuple(steps))
+        return LazyArray(self, tuple(call.shape), out_dt, tuple(leaves), head, tuple(steps), taps)
 
     def _try_fuse_unary(self, call, args):
         name = call.name
@@ -929,14 +970,44 @@ class GpuBackend(Backend):
             step = (64 + _lib.UNOP[name], 0, 0, 0, 0, 0.0)
         else:
             return None
-        leaves, head, steps = self._chain_from(a)
+        leaves, head, steps, taps = self._chain_from(a, call.shape)
         steps.append(step)
-        return LazyArray(self, tuple(call.shape), out_dt, tuple(leaves), head, tuple(steps))
+        return LazyArray(self, tuple(call.shape), out_dt, tuple(leaves), head, tuple(steps), taps)
+
+    def _lazy_result(self, lz):
+        if self._lazy_ok:
+            return lz
+        if self._lazy_tap and lz.dtype is dtypes.f32:
+            lz.tap_ok = True  # stays pending: its first (elementwise) consumer's kernel stores it
+            return lz
+        return lz.dev()
 
     def _run_chain(self, lz):
         out = self._new(lz.shape, lz.dtype, "fused")
         if out.block is None:
             return out
+        taps = [(k, t) for k, t in lz.taps if t._dev is None]
+        if taps:
+            if any(type(d) is LazyWindow and d._dev is None for d in lz.leaves):
+                for _, t in taps:
+                    t.dev()  # (windowed chains have no taps: run the intermediates alone)
+            else:
+                bufs = [self._new(t.shape, t.dtype, "fused") for _, t in taps]
+                steps = b"".join(_lib.STEP.pack(op, kind, side, leaf, tb, 0, sc)
+                                 for op, kind, side, leaf, tb, sc in lz.steps)
+                hk, hv = (0, 0.0) if lz.head[0] == "leaf" else (1, float(lz.head[1]))
+                after = struct.pack(f"<{len(taps)}i", *(k for k, _ in taps))
+                rc = self._lib.pb_ew_chain_taps(len(lz.leaves), b"".join(d.packed() for d in lz.leaves), hk, hv,
+                                                len(lz.steps), steps, len(taps), after,
+                                                b"".join(b.packed() for b in bufs), out.packed())
+                if rc != _lib.UNSUPPORTED:
+                    _lib.check(rc, "fused elementwise chain (taps)")
+                    for (_, t), b in zip(taps, bufs):
+                        t._dev = b
+                        t.leaves = t.steps = None
+                    return out
+                for _, t in taps:  # not specialisable (no NVRTC): the intermediates run alone
+                    t.dev()
         steps = b"".join(_lib.STEP.pack(op, kind, side, leaf, tb, 0, sc) for op, kind, side, leaf, tb, sc in lz.steps)
         hk, hv = (0, 0.0) if lz.head[0] == "leaf" else (1, float(lz.head[1]))
         if any(type(d) is LazyWindow and d._dev is None for d in lz.leaves):
@@ -977,7 +1048,7 @@ class GpuBackend(Backend):
                            (len(args) > 1 and type(args[1]) in _CHAINABLE)):
             lz = self._try_fuse_binary(call, args)
             if lz is not None:
-                return lz if self._lazy_ok else lz.dev()
+                return self._lazy_result(lz)
         args = [a.dev() if type(a) in _CHAINABLE else a for a in args]
         out = self._new(tuple(call.shape), call.dtype, name)
         if out.block is None:
@@ -1052,7 +1123,7 @@ class GpuBackend(Backend):
         if self._fuse and (self._lazy_ok or self._planned or type(args[0]) in _CHAINABLE):
             lz = self._try_fuse_unary(call, args)
             if lz is not None:
-                return lz if self._lazy_ok else lz.dev()
+                return self._lazy_result(lz)
         args = [a.dev() if type(a) in _CHAINABLE else a for a in args]
         a = args[0]
         out = self._new(tuple(call.shape), call.dtype, call.name)

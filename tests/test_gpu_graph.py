@@ -70,6 +70,26 @@ def test_planned_fusion_bit_identical_and_fewer_launches(name, shape, classes):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("name,shape,classes", [("lenet", (1, 28, 28), 10), ("resnet_tiny", (3, 32, 32), 10)])
+def test_chain_taps_bit_identical_and_fewer_launches(name, shape, classes, monkeypatch):
+    """Taps (pb_ew_chain_taps): a multi-use elementwise intermediate -- BatchNorm's xhat, the
+    affine output before the ReLU -- is stored by its first consumer's chain kernel instead of
+    a pass of its own.  Same losses and state bit for bit, fewer launches than without taps."""
+    from paper_2201_12465_b200.gpu import backend as gb
+    be = gpu_backend()
+    monkeypatch.setattr(gb, "_TAPS", False)
+    off = _run(name, be, True, 6, 4, shape, classes, fuse=True)
+    monkeypatch.setattr(gb, "_TAPS", True)
+    on = _run(name, be, True, 6, 4, shape, classes, fuse=True)
+    assert on[4].plan_abandoned is False
+    if name == "resnet_tiny":  # (LeNet has no BatchNorm chains to tap)
+        assert on[4].launches < off[4].launches, (on[4].launches, off[4].launches)
+    assert on[4].launches <= off[4].launches
+    assert on[0] == off[0], (on[0], off[0])
+    for a, b in zip(off[1] + off[2] + off[3], on[1] + on[2] + on[3]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("fuse", [False, True])
 def test_captured_dropout_draws_fresh_masks_bit_identical(fuse):
     """Dropout (minml/nn.py:247-256) inside the graph: each replay draws the counter range the
