@@ -2181,12 +2181,42 @@ __device__ __forceinline__ void rc_mul_batch(const RCArgs& p, const int64_t (&of
   }
 }
 
-// SRC 1: plain source; 2: product source; 0: the interpreter
+// one-step source (round 2): one f32 leaf and one cheap step -- neg / abs, or add / sub / mul
+// with a scalar (the sub backward's -g before its _unbroadcast sum); the same functors
+__device__ __forceinline__ float rc_one(const ChainStep& st, float a) {
+  if (st.kind == 0) return st.op - 64 == PB_NEG ? Un<PB_NEG, float>::f(a) : Un<PB_ABS, float>::f(a);
+  const float x = st.side ? st.scalar : a, y = st.side ? a : st.scalar;
+  return st.op == PB_ADD ? Bin<PB_ADD, float>::f(x, y)
+                         : st.op == PB_SUB ? Bin<PB_SUB, float>::f(x, y) : Bin<PB_MUL, float>::f(x, y);
+}
+template <int B, bool V4>
+__device__ __forceinline__ void rc_one_batch(const RCArgs& p, const int64_t (&off)[B][1], const bool (&on)[B],
+                                             float4 (&v)[B]) {
+  const float* f = (const float*)p.leaf[0];
+  const bool vec = V4 && p.s_vec[0];
+  const ChainStep st = p.step[0];
+#pragma unroll
+  for (int u = 0; u < B; ++u) {
+    if (!on[u]) continue;
+    if (vec) {
+      v[u] = __ldg(reinterpret_cast<const float4*>(f + off[u][0]));
+    } else {
+      const float q = __ldg(f + off[u][0]);
+      v[u] = make_float4(q, q, q, q);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < B; ++u)
+    v[u] = make_float4(rc_one(st, v[u].x), rc_one(st, v[u].y), rc_one(st, v[u].z), rc_one(st, v[u].w));
+}
+
+// SRC 1: plain source; 2: product source; 3: one-step source; 0: the interpreter
 template <int NL, int B, bool V4, int SRC>
 __device__ __forceinline__ void rc_source(const RCArgs& p, const int64_t (&off)[B][NL], const bool (&on)[B],
                                           float4 (&v)[B]) {
   if constexpr (SRC == 1) rc_load_batch<B, V4>(p, off, on, v);
   else if constexpr (SRC == 2) rc_mul_batch<NL, B, V4>(p, off, on, v);
+  else if constexpr (SRC == 3) rc_one_batch<B, V4>(p, off, on, v);
   else rc_eval_batch<NL, B, V4>(p, off, on, v);
 }
 
@@ -2227,7 +2257,7 @@ __global__ void __launch_bounds__(256) redchain_rows(RCArgs p) {
   const int i3a = sp * p.r3, np = min(p.r3, p.E3 - i3a);
   int64_t gb[NL];
   rc_group_base<NL>(p, g, gb);
-  constexpr int B = SRC == 1 ? 8 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
+  constexpr int B = SRC == 1 || SRC == 3 ? 8 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
   const int units = np * p.E2 * p.U1;
   for (int u0 = threadIdx.x; u0 < units; u0 += B * blockDim.x) {
     float4 v[B];
@@ -2344,7 +2374,7 @@ __global__ void __launch_bounds__(256) redchain_cols(RCArgs p) {
       int64_t po[NL];
 #pragma unroll
       for (int l = 0; l < NL; ++l) po[l] = gb[l] + (int64_t)i3 * p.s3[l] + (int64_t)(h0 + hl) * p.s2[l];
-      constexpr int B = SRC == 1 ? 16 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
+      constexpr int B = SRC == 1 ? 16 : SRC == 3 ? 8 : SRC == 2 ? (NL == 1 ? 8 : 4) : (NL <= 3 ? 4 : 2);
       for (int j = j0; j < j1; j += B) {
         float4 v[B];
         int64_t off[B][NL];
@@ -2852,8 +2882,13 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
   const bool product = !interp_only && nsteps == 1 && head_kind == 0 && steps[0].op == PB_MUL &&
                        ((nleaves == 1 && steps[0].kind == 3) || (nleaves == 2 && steps[0].kind == 1 && steps[0].leaf == 1)) &&
                        !p.is_bool[0] && (nleaves == 1 || !p.is_bool[1]);
-  switch (plain ? 0 : product ? -nleaves : nleaves) {
+  const int so = nsteps == 1 ? steps[0].op : -1, sk = nsteps == 1 ? steps[0].kind : -1;
+  const bool one = !interp_only && nleaves == 1 && nsteps == 1 && head_kind == 0 && !p.is_bool[0] &&
+                   ((sk == 0 && (so == 64 + PB_NEG || so == 64 + PB_ABS)) ||
+                    (sk == 2 && (so == PB_ADD || so == PB_SUB || so == PB_MUL)));
+  switch (plain ? 0 : product ? -nleaves : one ? -3 : nleaves) {
     case 0: launch_redchain<1, 1>(p, rows, v4, (int)grid, threads, smem, s); break;
+    case -3: launch_redchain<1, 3>(p, rows, v4, (int)grid, threads, smem, s); break;
     case -1: launch_redchain<1, 2>(p, rows, v4, (int)grid, threads, smem, s); break;
     case -2: launch_redchain<2, 2>(p, rows, v4, (int)grid, threads, smem, s); break;
     case 1: launch_redchain<1, 0>(p, rows, v4, (int)grid, threads, smem, s); break;
