@@ -2826,9 +2826,13 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
     // whole groups in one block (no ticket) when there are enough groups to fill the SMs, else
     // split the planes so that ~4 blocks per SM run; shared memory caps the planes per block
     const int64_t plane = (int64_t)p.E2 * p.E1p;
-    const int64_t target = 4 * (int64_t)num_sms();
+    // planes per block: a 48 KB plane budget (4 blocks per SM) measured best -- 96 KB: +0.16 ms per
+    // ResNet-50 step, 12-24 KB: more tickets and tail (profiles/r2/experiments/rc_smem_sweep.txt)
+    static const int64_t budget = getenv("PB_RC_SMEM_KB") ? atoi(getenv("PB_RC_SMEM_KB")) : 48;  // experiment hooks
+    static const int64_t tgt = getenv("PB_RC_TARGET") ? atoi(getenv("PB_RC_TARGET")) : 4;
+    const int64_t target = tgt * (int64_t)num_sms();
     int64_t pp = G * 2 >= target ? p.E3 : (p.E3 + (target + G - 1) / G - 1) / ((target + G - 1) / G);
-    const int64_t cap = (96 * 1024 / 4 - 2 * (int64_t)p.E3 * (p.E2 + 1)) / plane;
+    const int64_t cap = (budget * 1024 / 4 - 2 * (int64_t)p.E3 * (p.E2 + 1)) / plane;
     if (pp > cap) pp = cap > 1 ? cap : 1;
     if (pp > p.E3) pp = p.E3;
     if (pp < 1) pp = 1;
@@ -2847,7 +2851,8 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
     // one pass of <= 256 (row, column-unit) pairs per block, and >= ~4 blocks per SM: few groups
     // split their rows further (the threads then split the stage-1 axis into slices)
     const int wu = p.E3 / unit;
-    int hr = wu >= 256 ? 1 : 256 / wu;  // one pass of <= 256 (row, column-unit) pairs per block
+    static const int pairs = getenv("PB_RC_COLS_PAIRS") ? atoi(getenv("PB_RC_COLS_PAIRS")) : 256;  // experiment hook
+    int hr = wu >= pairs ? 1 : pairs / wu;  // one pass of <= `pairs` (row, column-unit) pairs per block
     if (hr > p.E2) hr = p.E2;
     r3 = hr;
     nsplit = (p.E2 + hr - 1) / hr;
