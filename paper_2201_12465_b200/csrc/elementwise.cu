@@ -1306,7 +1306,9 @@ static unsigned jit_grid(CUfunction fn, uint32_t units) {
     auto it = j.resident.find(fn);
     if (it != j.resident.end()) b = it->second;
   }
-  const uint64_t need = ((uint64_t)units + 255) / 256, wave = (uint64_t)num_sms() * b;
+  static const int waves = getenv("PB_JIT_WAVES") ? atoi(getenv("PB_JIT_WAVES")) : 1;  // experiment hook (0: no cap)
+  const uint64_t need = ((uint64_t)units + 255) / 256, wave = (uint64_t)num_sms() * b * (waves > 0 ? waves : 1);
+  if (waves <= 0) return (unsigned)(need ? (need < 0x7fffffffu ? need : 0x7fffffffu) : 1);
   return (unsigned)(need < wave ? (need ? need : 1) : wave);
 }
 
@@ -2812,8 +2814,9 @@ int pb_reduce_chain(int nleaves, const pb_tensor* leaves, int head_kind, double 
   bool heavy = nleaves > 2;
   for (int k = 0; k < nsteps; ++k) heavy = heavy || (steps[k].kind != 0 && steps[k].op == PB_DIV);
   if (!all_sizes && heavy) return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: heavy chain");
+  static const bool plain_rows = getenv("PB_RC_PLAIN_ROWS") != nullptr;  // experiment hook: fused plain rows
   if (!all_sizes && nleaves == 1 && nsteps == 0 && head_kind == 0 &&
-      (rows ? !(G < 256 || numel4 < ((int64_t)1 << 21)) : !(v4 && numel4 < ((int64_t)1 << 22))))
+      (rows ? !(plain_rows || G < 256 || numel4 < ((int64_t)1 << 21)) : !(v4 && numel4 < ((int64_t)1 << 22))))
     return fail(PB_ERR_UNSUPPORTED, "pb_reduce_chain: plain source streams faster stage by stage");
   // rows: a block owns one group and `pp` planes (>= ~2K elements); cols: one group and `hr` rows
   // of stage 2 (~256 threads of work)
