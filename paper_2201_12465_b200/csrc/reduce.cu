@@ -12,6 +12,7 @@
 // chunk order, so the result is deterministic run to run.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <type_traits>
 #include "common.cuh"
 
@@ -530,7 +531,8 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int ep
     r.chunks = 1;
     r.chunk = r.R;
     r.partial = nullptr;
-    const int rows = r.R <= 32 ? 256 : r.R <= 64 ? 128 : 64;
+    static const int rdiv = getenv("PB_RED_ROWS_DIV") ? atoi(getenv("PB_RED_ROWS_DIV")) : 1;  // experiment hook
+    const int rows = (r.R <= 32 ? 256 : r.R <= 64 ? 128 : 64) / (rdiv > 0 ? rdiv : 1);
     const size_t smem = (size_t)rows * r.R * 4;
     static bool attr = false;
     if (!attr) {
@@ -556,7 +558,8 @@ static int run_reduce(const pb_tensor* a, int axis, const pb_tensor* out, int ep
       r.chunk = r.R;
       r.partial = nullptr;
       const int64_t threads = r.O / 4;
-      if (threads >= (int64_t)num_sms() * 512 || r.R < 16) {  // enough outputs: one thread walks all of R
+      static const int64_t thr = getenv("PB_RED_COLS_THR") ? atoll(getenv("PB_RED_COLS_THR")) : 512;  // experiment hook
+      if (threads >= (int64_t)num_sms() * thr || r.R < 16) {  // enough outputs: one thread walks all of R
         const int64_t blocks = (threads + 255) / 256;
         const int grid = (int)(blocks < (int64_t)num_sms() * 8 ? blocks : (int64_t)num_sms() * 8);
         red_cols4_sum<<<grid, 256, 0, s>>>(r);
