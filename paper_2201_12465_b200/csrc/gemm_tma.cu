@@ -812,6 +812,15 @@ using namespace pb::tma;
 
 static int g_tma = 1;
 
+// 1x1 convs over more pixels than this stay on gemm_tc.cu.  Round 1 measured 56x56 planes (b32)
+// losing to the hi/lo pre-pass; with round 2's MMA issue loop and drains the TMA kernel wins
+// there too (ResNet-50 step 23.52 -> 23.48 ms, profiles/r2/experiments/conv_route_sweep.txt),
+// so there is no limit by default; PB_TMA_1X1_MAXPIX sets one (experiment hook)
+static int64_t max_1x1_pixels() {
+  static const int64_t v = getenv("PB_TMA_1X1_MAXPIX") ? atoll(getenv("PB_TMA_1X1_MAXPIX")) : ((int64_t)1 << 40);
+  return v;
+}
+
 // strided k x k dgrad by sub-pixel decomposition: output pixel (s*a + ah, s*b + aw) only meets
 // taps r = ah + p (mod s), at gradient row a + (ah + p - r) / s.  Each of the s*s classes is a
 // stride-1 correlation of g (NHWC planes, shared) with its own sub-kernel and asymmetric halo,
@@ -923,7 +932,7 @@ int pb_conv2d_tma(const pb_tensor* x, const pb_tensor* w, const pb_tensor* bias,
   if (!geometry_ok(pr) || F == 0 || N == 0) return PB_ERR_UNSUPPORTED;
   // 1x1 convs over large planes are bound by the hi/lo pre-pass (measured: 56x56 at b32
   // runs faster on gemm_tc.cu, which reads x once); 3x3 and the smaller planes win here
-  if (KH * KW == 1 && (int64_t)N * H * W > 25088) return PB_ERR_UNSUPPORTED;
+  if (KH * KW == 1 && (int64_t)N * H * W > max_1x1_pixels()) return PB_ERR_UNSUPPORTED;
   const int64_t act = (int64_t)N * C * H * W, K = (int64_t)C * KH * KW, rows = (int64_t)N * pr.HO * pr.WO;
   if (!fits(act) || !fits(rows * F) || !fits(K * F) || F % 4 != 0) return PB_ERR_UNSUPPORTED;
   pr.F = F;
@@ -1019,7 +1028,7 @@ int pb_conv2d_grad_input_tma(const pb_tensor* gr, const pb_tensor* w, const pb_c
   // the "conv" runs over g [N, F, HO, WO] and produces [N, Cx, H, W]
   Prob pr = make_prob(N, HO, WO, F, KH, KW, 1, 1, ph, pw);
   if (!geometry_ok(pr) || pr.HO != H || pr.WO != W || Cx == 0 || N == 0 || Cx % 4 != 0) return PB_ERR_UNSUPPORTED;
-  if (KH * KW == 1 && (int64_t)N * H * W > 25088) return PB_ERR_UNSUPPORTED;  // as in fprop
+  if (KH * KW == 1 && (int64_t)N * H * W > max_1x1_pixels()) return PB_ERR_UNSUPPORTED;  // as in fprop
   const int64_t act = (int64_t)N * F * HO * WO, K = (int64_t)F * KH * KW, rows = (int64_t)N * H * W;
   if (!fits(act) || !fits(rows * Cx) || !fits(K * Cx)) return PB_ERR_UNSUPPORTED;
   pr.F = Cx;
