@@ -1075,7 +1075,8 @@ int pb_conv2d_grad_weight_tma(const pb_tensor* x, const pb_tensor* gr, const pb_
       force = e && e[0] == '2';
     }
     const int64_t P = (int64_t)N * HO * pr.WO;
-    const bool win = P <= 6272 || (P <= 25088 && (RS > 1 || (int64_t)C * F >= 131072));
+    static const int64_t p2 = getenv("PB_TMA_WG_P2") ? atoll(getenv("PB_TMA_WG_P2")) : 25088;  // experiment hook
+    const bool win = P <= 6272 || (P <= p2 && (RS > 1 || (int64_t)C * F >= 131072));
     if (!force && !win) return PB_ERR_UNSUPPORTED;
   }
   pr.Wp = (W + 2 * pad + 3) / 4 * 4;
