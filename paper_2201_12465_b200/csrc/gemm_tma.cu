@@ -1262,7 +1262,8 @@ int pb_matmul_tma(const pb_tensor* a, const pb_tensor* b, const pb_tensor* out) 
   const int64_t M = a->shape[0], K = a->shape[1], N = b->shape[1];
   // measured in CUDA graphs (tools/mm_table.py): the operand pre-pass pays off once M >= 256;
   // for the b128 classifier GEMMs (M = 128, multi-MB weights) gemm_tc.cu's in-GEMM split wins
-  if (M < 256 || N < 64 || K < 64 || !fits(M * N) || !fits(M * K) || !fits(N * K)) return PB_ERR_UNSUPPORTED;
+  static const int64_t min_m = getenv("PB_TMA_MM_MIN_M") ? atoll(getenv("PB_TMA_MM_MIN_M")) : 256;  // experiment hook
+  if (M < min_m || N < 64 || K < 64 || !fits(M * N) || !fits(M * K) || !fits(N * K)) return PB_ERR_UNSUPPORTED;
   const int64_t kp = (K + 3) / 4 * 4;
   const int BN = M <= 64 ? 64 : 128;
   Prob pr{};
