@@ -165,7 +165,11 @@ class LazyArray:
 _FUSE_BIN = {"add", "sub", "mul", "div", "pow", "minimum", "maximum", "eq", "lt", "gt", "logical_and", "logical_or"}
 _FUSE_UN = {"neg", "abs", "exp", "log", "sqrt", "sin", "cos", "tanh", "logical_not", "astype"}
 _MAX_LEAVES, _MAX_STEPS = 8, 16
-_MAX_USES = int(os.environ.get("PB_FUSE_USES", "1"))  # consumers that may recompute one chain
+# consumers that may extend (recompute) one pending chain.  2 makes the device step faster
+# (23.47 -> 23.17 ms: a tapped intermediate's second consumer recomputes it inline) but the
+# pipelined e2e run became unstable (23.35 / 26.60 ms on repeats, against 23.51 / 23.51 with 1;
+# profiles/r2/experiments/fuse_uses_sweep.txt), so 1 stays until that is understood
+_MAX_USES = int(os.environ.get("PB_FUSE_USES", "1"))
 _MAX_TAPS = 4
 _TAPS = os.environ.get("PB_FUSE_TAPS", "1") != "0"  # experiment hook: 0 materialises multi-use chains alone
 
