@@ -1,5 +1,7 @@
 """The measured unit of work: one optimizer step (semantics of minml/training.py:30-51)."""
 
+import collections
+import gc
 import json
 import struct
 
@@ -217,18 +219,33 @@ class CapturedStep:
 
         Once the graph is recorded, batch i+1's host->device copy runs on the copy stream
         while step i computes, and step i's loss comes back through a posted pinned read
-        that the host collects after queueing step i+1, so the compute stream never waits
+        that the host collects after queueing step i+2, so the compute stream never waits
         for the host.  Every step still copies its whole batch in and its loss out.  Batches
         in page-locked memory (``GpuBackend.pinned``) go over in one DMA; a batch's host
         buffers may be reused once the loss of the step before it has been yielded.
         """
+        # Python's cyclic collector is paused while steps run (reference counting still frees
+        # everything acyclic): a full collection walks every live object, and the recorded step
+        # keeps many alive.  Restored when the generator finishes or is closed.
+        paused = gc.isenabled()
+        if paused:
+            gc.disable()
+        try:
+            yield from self._run(batches)
+        finally:
+            if paused:
+                gc.enable()
+
+    def _run(self, batches):
         be = self.backend
-        pending, k = None, 0
+        # two steps stay queued ahead of the host: a host stall shorter than a step then never
+        # idles the device (with one step ahead the pipelined e2e time varied 23.5-33.7 ms/step
+        # between identical runs, tools/e2e_diag.py; the graph-only replay stayed at 23.5)
+        pending, k = collections.deque(), 0
         for images, labels in batches:
             if self.graph is not None and self._signature() != self._sig:
-                if pending is not None:
-                    yield float(be.fetch_read(*pending).reshape(()))
-                    pending = None
+                while pending:
+                    yield float(be.fetch_read(*pending.popleft()).reshape(()))
                 self.graph = None
             if self.graph is None:
                 yield self(images, labels)[0]
@@ -253,16 +270,16 @@ class CapturedStep:
             self.graph.launch()
             loss = self.loss.data if isinstance(self.loss, Variable) else self.loss
             meta = be.post_read(loss, k % 8)
-            if pending is not None:
-                value = float(be.fetch_read(*pending).reshape(()))
-                # step k-1 is done, so this batch's copy (queued behind it) is about to land:
-                # wait for it, then the caller may reuse the host buffers of this batch
+            pending.append((k % 8, meta))
+            if len(pending) > 2:
+                value = float(be.fetch_read(*pending.popleft()).reshape(()))
+                # step k-2 is done, so this batch's copy (queued behind step k-1's input copy)
+                # is about to land: wait for it, then the caller may reuse its host buffers
                 be.stream_sync(2)
                 yield value
-            pending = (k % 8, meta)
             k += 1
-        if pending is not None:
-            yield float(be.fetch_read(*pending).reshape(()))
+        while pending:
+            yield float(be.fetch_read(*pending.popleft()).reshape(()))
 
     def _capture(self):
         be = self.backend
