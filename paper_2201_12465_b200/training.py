@@ -12,6 +12,9 @@ from . import nn, optim, registry
 from .autograd import Variable
 from .errors import FormatError
 
+# steps CapturedStep.run keeps queued ahead of the host (losses are collected this many steps late)
+_AHEAD = 3
+
 
 def model_backend(model):
     params = model.params()
@@ -219,7 +222,7 @@ class CapturedStep:
 
         Once the graph is recorded, batch i+1's host->device copy runs on the copy stream
         while step i computes, and step i's loss comes back through a posted pinned read
-        that the host collects after queueing step i+2, so the compute stream never waits
+        that the host collects after queueing step i+3, so the compute stream never waits
         for the host.  Every step still copies its whole batch in and its loss out.  Batches
         in page-locked memory (``GpuBackend.pinned``) go over in one DMA; a batch's host
         buffers may be reused once the loss of the step before it has been yielded.
@@ -238,8 +241,8 @@ class CapturedStep:
 
     def _run(self, batches):
         be = self.backend
-        # two steps stay queued ahead of the host: a host stall shorter than a step then never
-        # idles the device (with one step ahead the pipelined e2e time varied 23.5-33.7 ms/step
+        # _AHEAD steps stay queued ahead of the host: a host stall shorter than that many steps
+        # never idles the device (with one step ahead the pipelined e2e time varied 23.5-33.7 ms/step
         # between identical runs, tools/e2e_diag.py; the graph-only replay stayed at 23.5)
         pending, k = collections.deque(), 0
         for images, labels in batches:
@@ -271,10 +274,10 @@ class CapturedStep:
             loss = self.loss.data if isinstance(self.loss, Variable) else self.loss
             meta = be.post_read(loss, k % 8)
             pending.append((k % 8, meta))
-            if len(pending) > 2:
+            if len(pending) > _AHEAD:
                 value = float(be.fetch_read(*pending.popleft()).reshape(()))
-                # step k-2 is done, so this batch's copy (queued behind step k-1's input copy)
-                # is about to land: wait for it, then the caller may reuse its host buffers
+                # an earlier step is done and this batch's copy is queued behind the inputs of the
+                # steps before it: wait for it to land, then the caller may reuse its host buffers
                 be.stream_sync(2)
                 yield value
             k += 1
