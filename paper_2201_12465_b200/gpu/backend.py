@@ -165,11 +165,10 @@ class LazyArray:
 _FUSE_BIN = {"add", "sub", "mul", "div", "pow", "minimum", "maximum", "eq", "lt", "gt", "logical_and", "logical_or"}
 _FUSE_UN = {"neg", "abs", "exp", "log", "sqrt", "sin", "cos", "tanh", "logical_not", "astype"}
 _MAX_LEAVES, _MAX_STEPS = 8, 16
-# consumers that may extend (recompute) one pending chain.  2 makes the device step faster
-# (23.47 -> 23.17 ms: a tapped intermediate's second consumer recomputes it inline) but the
-# pipelined e2e run became unstable (23.35 / 26.60 ms on repeats, against 23.51 / 23.51 with 1;
-# profiles/r2/experiments/fuse_uses_sweep.txt), so 1 stays until that is understood
-_MAX_USES = int(os.environ.get("PB_FUSE_USES", "1"))
+# consumers that may extend (recompute) one pending chain: 2 -- a tapped intermediate's second
+# elementwise consumer recomputes it inline instead of waiting for a pass of its own (ResNet-50
+# 23.47 -> 23.17 ms device, 23.51 -> 23.20 ms e2e; profiles/r2/experiments/fuse_uses_sweep.txt)
+_MAX_USES = int(os.environ.get("PB_FUSE_USES", "2"))
 _MAX_TAPS = 4
 _TAPS = os.environ.get("PB_FUSE_TAPS", "1") != "0"  # experiment hook: 0 materialises multi-use chains alone
 
