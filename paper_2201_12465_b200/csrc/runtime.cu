@@ -216,8 +216,13 @@ int pb_d2h_post(uint64_t src, uint64_t nbytes, int slot) {
   if (slot < 0 || slot >= kPostSlots || nbytes > kPostBytes) return fail(PB_ERR_ARG, "pb_d2h_post: bad slot or size");
   Post& p = g_post[slot];
   if (!p.host) {
-    PB_CUDA(cudaHostAlloc(&p.host, kPostBytes, cudaHostAllocDefault));
-    PB_CUDA(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+    // every slot at once: a page-locked allocation is slow and can stall the host, which must
+    // not happen inside a pipelined run that first touches slot k at step k
+    for (int i = 0; i < kPostSlots; ++i) {
+      if (g_post[i].host) continue;
+      PB_CUDA(cudaHostAlloc(&g_post[i].host, kPostBytes, cudaHostAllocDefault));
+      PB_CUDA(cudaEventCreateWithFlags(&g_post[i].ev, cudaEventDisableTiming));
+    }
   }
   if (nbytes) PB_CUDA(cudaMemcpyAsync(p.host, (const void*)(uintptr_t)src, nbytes, cudaMemcpyDeviceToHost, g_streams[0]));
   PB_CUDA(cudaEventRecord(p.ev, g_streams[0]));
